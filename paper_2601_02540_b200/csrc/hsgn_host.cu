@@ -1,0 +1,1253 @@
+// hsgn_host.cu -- host runtime of the B200 hot path and its C ABI
+// (include/hsgn_b200.h).
+//
+// Owns: the device context (RhsContext analogue, rhs.hpp:17-54), device
+// states with the slab layout, the fused BS3 driver (adaptive_solve,
+// time_integration.hpp:209-350) with CUDA-graph-captured fixed-step chunks,
+// the SBP-norm diagnostics, and the multi-GPU slab halo exchange over NCCL.
+// No CPU compute path exists: every operator launches sm_100a kernels.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <map>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/hsgn_b200.h"
+#include "sgn_device.cuh"
+
+namespace hsgn_dev {
+// sgn_stage.cu
+cudaError_t launch_stage(int mode, const StageArgs& A, cudaStream_t st);
+int stage_grid_blocks(const StageArgs& A);
+cudaError_t launch_sum_partials(const double* part, int n, double* out, cudaStream_t st);
+// sgn_aux.cu
+
+cudaError_t launch_row_sums(const AuxArgs& A, int kind, const double* q, const double* qt, int field,
+                            double* rows, cudaStream_t st);
+cudaError_t launch_depth_check(const double* h, long long n, unsigned long long* bad, cudaStream_t st);
+cudaError_t launch_axpy5(const double* a, double c, const double* x, double* out, long long n, long long fs,
+                         cudaStream_t st);
+int wrms_blocks();
+cudaError_t launch_wrms(const double* x, const double* ref, double atol, double rtol, long long n, long long fs,
+                        double* part, cudaStream_t st);
+cudaError_t launch_init_aux(const AuxArgs& A, double* q, cudaStream_t st);
+}  // namespace hsgn_dev
+
+using namespace hsgn_dev;
+
+// ------------------------------------------------------------------ NCCL (dlopen)
+// The slab exchange needs five NCCL entry points; they are resolved at run
+// time from the libnccl.so.2 already mapped by torch (or the system one), so
+// single-GPU use carries no NCCL dependency.
+namespace {
+typedef struct {
+    char internal[128];
+} nccl_uid;
+typedef void* nccl_comm;
+typedef int (*p_get_uid)(nccl_uid*);
+typedef int (*p_init_rank)(nccl_comm*, int, nccl_uid, int);
+typedef int (*p_send)(const void*, size_t, int, int, nccl_comm, cudaStream_t);
+typedef int (*p_recv)(void*, size_t, int, int, nccl_comm, cudaStream_t);
+typedef int (*p_group)(void);
+typedef int (*p_destroy)(nccl_comm);
+typedef const char* (*p_errstr)(int);
+struct NcclApi {
+    bool ok = false;
+    p_get_uid get_uid;
+    p_init_rank init_rank;
+    p_send send;
+    p_recv recv;
+    p_group group_start, group_end;
+    p_destroy destroy;
+    p_errstr errstr;
+};
+const NcclApi& nccl() {
+    static NcclApi api;
+    static bool tried = false;
+    if (tried) return api;
+    tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return api;
+    api.get_uid = (p_get_uid)dlsym(h, "ncclGetUniqueId");
+    api.init_rank = (p_init_rank)dlsym(h, "ncclCommInitRank");
+    api.send = (p_send)dlsym(h, "ncclSend");
+    api.recv = (p_recv)dlsym(h, "ncclRecv");
+    api.group_start = (p_group)dlsym(h, "ncclGroupStart");
+    api.group_end = (p_group)dlsym(h, "ncclGroupEnd");
+    api.destroy = (p_destroy)dlsym(h, "ncclCommDestroy");
+    api.errstr = (p_errstr)dlsym(h, "ncclGetErrorString");
+    api.ok = api.get_uid && api.init_rank && api.send && api.recv && api.group_start && api.group_end &&
+             api.destroy;
+    return api;
+}
+constexpr int NCCL_FLOAT64 = 8;  // ncclDouble
+}  // namespace
+
+// ------------------------------------------------------------------ types
+
+struct hsgn_state {
+    double* base = nullptr;  // 5 fields, each (ny_local + 2) rows of nx
+    long long fs = 0;        // field stride (elements)
+    double* f(int k) const { return base + k * fs; }
+};
+
+namespace {
+
+struct FixedGraph {
+    cudaGraphExec_t exec = nullptr;
+    int steps = 0;
+};
+
+}  // namespace
+
+struct hsgn_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    // global grid + slab
+    hsgn_grid grid{};
+    hsgn_phys phys{};
+    int j_begin = 0, j_end = 0, ny_loc = 0, rank = 0, nranks = 1;
+    double dx = 0, dy = 0;
+    long long fs = 0;  // elements per field incl. ghost rows
+    double* b = nullptr;  // bathymetry row 0 pointer (ghost rows allocated)
+    double* b_alloc = nullptr;
+    StageArgs base{};
+    AuxArgs aux{};
+    int source = 0;
+    int rows_per_block = 0;
+    int64_t n_evals = 0;
+    std::string err;
+    // workspace for the integrator
+    hsgn_state ws[8];  // y0,y1,k1a,k1b,k2,part,scratchA,scratchB
+    bool ws_ready = false;
+    StepRec* d_rec = nullptr;  // per-step records (capacity rec_cap)
+    int rec_cap = 0;
+    int* d_halt = nullptr;
+    double* d_err_part = nullptr;
+    int err_part_cap = 0;
+    double* d_scalar = nullptr;  // [0] err sum, [1..] misc
+    unsigned long long* d_bad = nullptr;
+    double* d_rows = nullptr;
+    double* h_rows = nullptr;
+    StepRec* h_rec = nullptr;
+    std::map<std::tuple<int, int, double, uint64_t, uint64_t>, FixedGraph> graphs;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    double last_ms = 0.0;
+    int64_t last_kernels = 0;
+    // NCCL
+    nccl_comm comm = nullptr;
+};
+
+namespace {
+
+hsgn_status fail(hsgn_ctx* c, hsgn_status s, const char* fmt, ...) {
+    if (c) {
+        char buf[512];
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(buf, sizeof buf, fmt, ap);
+        va_end(ap);
+        c->err = buf;
+    }
+    return s;
+}
+
+#define CK(call)                                                                               \
+    do {                                                                                       \
+        cudaError_t e_ = (call);                                                               \
+        if (e_ != cudaSuccess) return fail(c, HSGN_ECUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+    } while (0)
+
+bool is_pow2_ge1(double v) {
+    if (!(v >= 1.0) || !std::isfinite(v)) return false;
+    int e;
+    return std::frexp(v, &e) == 0.5;
+}
+
+double spacing(double lo, double hi, int n, int bounded) {  // grid.hpp:43-45
+    return bounded ? (hi - lo) / (n - 1) : (hi - lo) / n;
+}
+
+// Global y edge modes of a slab.
+void slab_edges(const hsgn_ctx* c, int* lo, int* hi) {
+    const bool yb = c->grid.kind_y == HSGN_BOUNDED;
+    if (c->nranks == 1) {
+        *lo = yb ? YE_CLAMP : YE_WRAP;
+        *hi = yb ? YE_CLAMP : YE_WRAP;
+        return;
+    }
+    *lo = (c->j_begin == 0 && yb) ? YE_CLAMP : YE_GHOST;
+    *hi = (c->j_end == c->grid.ny && yb) ? YE_CLAMP : YE_GHOST;
+}
+
+hsgn_status alloc_state(hsgn_ctx* c, hsgn_state* s) {
+    s->fs = c->fs;
+    CK(cudaMalloc(&s->base, sizeof(double) * 5 * c->fs));
+    CK(cudaMemsetAsync(s->base, 0, sizeof(double) * 5 * c->fs, c->stream));
+    s->base += c->grid.nx;  // row 0 of field 0 (row -1 is the ghost row)
+    return HSGN_OK;
+}
+
+}  // namespace
+
+// Freed pointer must be the allocation base (row -1 of field 0).
+static void free_state_c(hsgn_ctx* c, hsgn_state* s) {
+    if (s->base) cudaFree(s->base - c->grid.nx);
+    s->base = nullptr;
+}
+
+static hsgn_status setup_ctx(hsgn_ctx* c) {
+    const hsgn_grid& g = c->grid;
+    c->dx = spacing(g.x_min, g.x_max, g.nx, g.kind_x);
+    c->dy = spacing(g.y_min, g.y_max, g.ny, g.kind_y);
+    c->ny_loc = c->j_end - c->j_begin;
+    c->fs = (long long)(c->ny_loc + 2) * g.nx;
+    StageArgs& A = c->base;
+    std::memset(&A, 0, sizeof A);
+    A.nx = g.nx;
+    A.ny = c->ny_loc;
+    A.fs = c->fs;
+    slab_edges(c, &A.y_lo, &A.y_hi);
+    A.x_bounded = g.kind_x == HSGN_BOUNDED;
+    A.walls = (g.kind_x == HSGN_BOUNDED) || (g.kind_y == HSGN_BOUNDED);
+    A.sat_y_lo = g.kind_y == HSGN_BOUNDED && c->j_begin == 0;
+    A.sat_y_hi = g.kind_y == HSGN_BOUNDED && c->j_end == g.ny;
+    // sbp.hpp:46,63 (interior), :66 (closure), :254 (SAT); rhs.hpp:143-145
+    A.cpx = 1.0 / (2.0 * c->dx);
+    A.cpy = 1.0 / (2.0 * c->dy);
+    A.c1x = 1.0 / c->dx;
+    A.c1y = 1.0 / c->dy;
+    A.tdx = 2.0 / c->dx;
+    A.tdy = 2.0 / c->dy;
+    A.pow2 = is_pow2_ge1(A.cpx) && is_pow2_ge1(A.cpy) && A.c1x == 2.0 * A.cpx && A.c1y == 2.0 * A.cpy;
+    A.g = c->phys.g;
+    A.lambda = c->phys.lambda;
+    A.lam_half = c->phys.lambda / 2.0;
+    A.lam_third = c->phys.lambda / 3.0;
+    A.lam_sixth = c->phys.lambda / 6.0;
+    A.x_min = g.x_min;
+    A.y_min = g.y_min;
+    A.dx = c->dx;
+    A.dy = c->dy;
+    A.j_global0 = c->j_begin;
+    A.b = c->b;
+    A.h_floor = c->phys.h_floor;
+    // default launch shape: rows per CTA so that the grid is >= ~6 waves
+    A.rows_per_block = c->rows_per_block > 0 ? c->rows_per_block : 0;
+    if (A.rows_per_block <= 0) {
+        const int tiles_x = (g.nx + 127) / 128;
+        int rpb = 128;
+        while (rpb > 16 && (long long)tiles_x * ((c->ny_loc + rpb - 1) / rpb) < 148LL * 3 * 6) rpb /= 2;
+        A.rows_per_block = rpb;
+    }
+    AuxArgs& X = c->aux;
+    X.nx = g.nx;
+    X.ny = c->ny_loc;
+    X.fs = c->fs;
+    X.y_lo = A.y_lo;
+    X.y_hi = A.y_hi;
+    X.x_bounded = A.x_bounded;
+    X.y_bounded_lo = A.y_lo == YE_CLAMP;
+    X.y_bounded_hi = A.y_hi == YE_CLAMP;
+    X.pow2 = A.pow2;
+    X.dx = c->dx;
+    X.cpx = A.cpx;
+    X.cpy = A.cpy;
+    X.c1x = A.c1x;
+    X.c1y = A.c1y;
+    X.g = c->phys.g;
+    X.lambda = c->phys.lambda;
+    X.b = c->b;
+    return HSGN_OK;
+}
+
+// ------------------------------------------------------------------ halo exchange
+
+// After a stage wrote `s` (rows 0..ny_loc-1), fill the neighbours' ghost rows:
+// send row 0 to rank-1 (its row ny_loc ghost) and row ny_loc-1 to rank+1;
+// receive into our rows -1 / ny_loc.  One grouped NCCL call per exchange, on
+// the context stream (graph-capturable).
+static hsgn_status exchange(hsgn_ctx* c, const hsgn_state* s, int nfields) {
+    if (c->nranks == 1) return HSGN_OK;
+    if (!c->comm) return fail(c, HSGN_ENCCL, "slab context has no NCCL communicator attached");
+    const NcclApi& N = nccl();
+    const int nx = c->grid.nx;
+    const bool yb = c->grid.kind_y == HSGN_BOUNDED;
+    const int up = c->rank + 1 < c->nranks ? c->rank + 1 : (yb ? -1 : 0);
+    const int dn = c->rank > 0 ? c->rank - 1 : (yb ? -1 : c->nranks - 1);
+    int r = N.group_start();
+    for (int f = 0; f < nfields && r == 0; ++f) {
+        double* fld = s->f(f);
+        if (dn >= 0) {
+            r |= N.send(fld, nx, NCCL_FLOAT64, dn, c->comm, c->stream);
+            r |= N.recv(fld - nx, nx, NCCL_FLOAT64, dn, c->comm, c->stream);
+        }
+        if (up >= 0) {
+            r |= N.send(fld + (long long)(c->ny_loc - 1) * nx, nx, NCCL_FLOAT64, up, c->comm, c->stream);
+            r |= N.recv(fld + (long long)c->ny_loc * nx, nx, NCCL_FLOAT64, up, c->comm, c->stream);
+        }
+    }
+    r |= N.group_end();
+    if (r) return fail(c, HSGN_ENCCL, "ncclSend/Recv halo exchange failed (%d)", r);
+    return HSGN_OK;
+}
+
+// ------------------------------------------------------------------ stage launch helpers
+
+static StageArgs stage_args(hsgn_ctx* c, int mode, double t) {
+    StageArgs A = c->base;
+    (void)mode;
+    A.source = c->source;
+    A.t = t;
+    return A;
+}
+
+static hsgn_status launch(hsgn_ctx* c, int mode, const StageArgs& A) {
+    CK(launch_stage(mode, A, c->stream));
+    return HSGN_OK;
+}
+
+static hsgn_status ensure_recs(hsgn_ctx* c, int rec_cap);
+
+static hsgn_status ensure_ws(hsgn_ctx* c, int rec_cap) {
+    if (!c->ws_ready) {
+        for (int k = 0; k < 8; ++k) {
+            hsgn_status s = alloc_state(c, &c->ws[k]);
+            if (s) return s;
+        }
+        c->ws_ready = true;
+    }
+    return ensure_recs(c, rec_cap);
+}
+
+static hsgn_status ensure_recs(hsgn_ctx* c, int rec_cap) {
+    if (!c->d_halt) {
+        StageArgs A = c->base;
+        c->err_part_cap = stage_grid_blocks(A) + 1;
+        c->err_part_cap = std::max(c->err_part_cap, wrms_blocks());
+        CK(cudaMalloc(&c->d_err_part, sizeof(double) * c->err_part_cap));
+        CK(cudaMalloc(&c->d_scalar, sizeof(double) * 8));
+        CK(cudaMalloc(&c->d_halt, sizeof(int) * 4));
+    }
+    if (rec_cap > c->rec_cap) {
+        if (c->d_rec) cudaFree(c->d_rec);
+        if (c->h_rec) cudaFreeHost(c->h_rec);
+        CK(cudaMalloc(&c->d_rec, sizeof(StepRec) * rec_cap));
+        CK(cudaMallocHost(&c->h_rec, sizeof(StepRec) * rec_cap));
+        c->rec_cap = rec_cap;
+    }
+    return HSGN_OK;
+}
+
+static void reset_recs(hsgn_ctx* c, int n) {
+    // bad counters -> 0, minh -> all-ones ("none"), halt -> 0
+    cudaMemsetAsync(c->d_rec, 0xFF, sizeof(StepRec) * n, c->stream);
+    for (int s = 0; s < n; ++s) cudaMemsetAsync(&c->d_rec[s].bad[0], 0, sizeof(unsigned long long) * 3, c->stream);
+    cudaMemsetAsync(c->d_halt, 0, sizeof(int), c->stream);
+}
+
+// Enqueue one fused BS3 step (S1, S2, S3 + halo exchanges) on the stream.
+//   y, k1 : step inputs;  ynew, k4 : outputs;  k2 : scratch;  rec : this step's record
+//   prev  : previous step's record (halt check) or null
+static hsgn_status enqueue_step(hsgn_ctx* c, const hsgn_state* y, const hsgn_state* k1, hsgn_state* k2,
+                                hsgn_state* ynew, hsgn_state* k4, hsgn_state* part, StepRec* rec,
+                                const StepRec* prev, double t, double dt, bool adaptive, double atol,
+                                double rtol, int64_t* kernels) {
+    hsgn_status s;
+    // stage 1: k2 = f(t + dt/2, y + (dt/2) k1)
+    StageArgs A = stage_args(c, MODE_S1, t + 0.5 * dt);
+    A.a = 0.5 * dt;
+    A.y = y->base;
+    A.k = k1->base;
+    A.out = k2->base;
+    A.bad = &rec->bad[0];
+    A.halt = c->d_halt;
+    A.chk_bad = prev ? &prev->bad[2] : nullptr;
+    A.chk_minh = prev ? &prev->minh : nullptr;
+    if ((s = launch(c, MODE_S1, A))) return s;
+    if ((s = exchange(c, k2, 5))) return s;
+    // stage 2: k3 = f(t + 3dt/4, y + (3dt/4) k2); ynew = y + (2/9 dt) k1 + (1/3 dt) k2 + (4/9 dt) k3
+    A = stage_args(c, MODE_S2, t + 0.75 * dt);
+    A.a = 0.75 * dt;
+    A.c1 = dt * (2.0 / 9.0);
+    A.c2 = dt * (1.0 / 3.0);
+    A.c3 = dt * (4.0 / 9.0);
+    A.y = y->base;
+    A.k = k2->base;
+    A.kc = k1->base;
+    A.out = ynew->base;
+    A.adaptive = adaptive;
+    A.d1 = -5.0 / 72.0;
+    A.d2 = 1.0 / 12.0;
+    A.d3 = 1.0 / 9.0;
+    A.d4 = -1.0 / 8.0;
+    A.part = part ? part->base : nullptr;
+    A.bad = &rec->bad[1];
+    A.minh = &rec->minh;
+    A.halt = c->d_halt;
+    A.chk_bad = &rec->bad[0];
+    if ((s = launch(c, MODE_S2, A))) return s;
+    if ((s = exchange(c, ynew, 5))) return s;
+    // stage 3: k4 = f(t + dt, ynew) (FSAL)
+    A = stage_args(c, MODE_S3, t + dt);
+    A.y = ynew->base;
+    A.out = k4->base;
+    A.adaptive = adaptive;
+    A.d4 = -1.0 / 8.0;
+    A.dt = dt;
+    A.atol = atol;
+    A.rtol = rtol;
+    A.part = part ? part->base : nullptr;
+    A.yold = y->base;
+    A.err_part = c->d_err_part;
+    A.bad = &rec->bad[2];
+    A.halt = c->d_halt;
+    A.chk_bad = &rec->bad[1];
+    if ((s = launch(c, MODE_S3, A))) return s;
+    if ((s = exchange(c, k4, 5))) return s;
+    if (kernels) *kernels += 3;
+    return HSGN_OK;
+}
+
+// RHS evaluation into out (no depth pre-check): used by the integrator.
+static hsgn_status rhs_raw(hsgn_ctx* c, double t, const hsgn_state* q, hsgn_state* out, double lambda_override,
+                           bool shallow, unsigned long long* d_bad) {
+    StageArgs A = stage_args(c, MODE_RHS, t);
+    if (shallow) {
+        A.lambda = 0.0;
+        A.lam_half = 0.0;
+        A.lam_third = 0.0;
+        A.lam_sixth = 0.0;
+        A.shallow = 1;
+    }
+    (void)lambda_override;
+    A.y = q->base;
+    A.out = out->base;
+    A.bad = d_bad;
+    ++c->n_evals;
+    hsgn_status s = launch(c, MODE_RHS, A);
+    if (s) return s;
+    return exchange(c, out, 5);
+}
+
+static hsgn_status rhs_checked(hsgn_ctx* c, double t, const hsgn_state* q, hsgn_state* out, bool shallow,
+                               int64_t* bad_nodes) {
+    hsgn_status s = ensure_recs(c, 1);
+    if (s) return s;
+    unsigned long long* d_bad = &c->d_rec[0].bad[0];
+    CK(cudaMemsetAsync(d_bad, 0, sizeof(unsigned long long), c->stream));
+    CK(launch_depth_check(q->base, (long long)c->ny_loc * c->grid.nx, d_bad, c->stream));
+    unsigned long long hb = 0;
+    CK(cudaMemcpyAsync(&hb, d_bad, sizeof hb, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (bad_nodes) *bad_nodes = (int64_t)hb;
+    if (hb) {
+        ++c->n_evals;  // rhs.hpp:84 counts the evaluation before throwing
+        return fail(c, HSGN_EDEPTH, "tendency evaluation at t = %f: %llu nodes with non-positive depth", t, hb);
+    }
+    s = rhs_raw(c, t, q, out, 0.0, shallow, &c->d_rec[0].bad[1]);
+    if (s) return s;
+    CK(cudaStreamSynchronize(c->stream));
+    return HSGN_OK;
+}
+
+// ------------------------------------------------------------------ reductions
+
+static hsgn_status row_sums_dev(hsgn_ctx* c, int kind, const hsgn_state* q, const hsgn_state* qt, int field) {
+    if (!c->d_rows) {
+        CK(cudaMalloc(&c->d_rows, sizeof(double) * c->ny_loc));
+        CK(cudaMallocHost(&c->h_rows, sizeof(double) * c->ny_loc));
+    }
+    CK(launch_row_sums(c->aux, kind, q->base, qt ? qt->base : nullptr, field, c->d_rows, c->stream));
+    CK(cudaMemcpyAsync(c->h_rows, c->d_rows, sizeof(double) * c->ny_loc, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return HSGN_OK;
+}
+
+static double outer_sum(const hsgn_grid* g, const double* rows, int j_begin, int j_end) {
+    // sbp.hpp:232-237: Kahan over wy_j * row_j in row order
+    const double dy = spacing(g->y_min, g->y_max, g->ny, g->kind_y);
+    double sum = 0.0, comp = 0.0;
+    for (int j = j_begin; j < j_end; ++j) {
+        double wy = dy;
+        if (g->kind_y == HSGN_BOUNDED && (j == 0 || j == g->ny - 1)) wy = 0.5 * dy;
+        const double term = wy * rows[j - j_begin] - comp;
+        const double t = sum + term;
+        comp = (t - sum) - term;
+        sum = t;
+    }
+    return sum;
+}
+
+static hsgn_status reduce_full(hsgn_ctx* c, int kind, const hsgn_state* q, const hsgn_state* qt, int field,
+                               double* out) {
+    if (c->nranks != 1)
+        return fail(c, HSGN_EINVAL, "slab contexts reduce via hsgn_row_sums + hsgn_outer_sum");
+    hsgn_status s = row_sums_dev(c, kind, q, qt, field);
+    if (s) return s;
+    *out = outer_sum(&c->grid, c->h_rows, 0, c->grid.ny);
+    return HSGN_OK;
+}
+
+// ------------------------------------------------------------------ C ABI
+
+extern "C" {
+
+const char* hsgn_build_info(void) {
+    return "hsgn_b200: fused fp64 SGN split-form stage kernels, sm_100a, --fmad=false";
+}
+
+static hsgn_status create_common(const hsgn_grid* grid, const hsgn_phys* phys, const double* b_host, int device,
+                                 int j_begin, int j_end, int rank, int nranks, hsgn_ctx** out) {
+    if (!grid || !phys || !b_host || !out) return HSGN_EINVAL;
+    *out = nullptr;
+    hsgn_ctx* c = new hsgn_ctx();
+    c->grid = *grid;
+    c->phys = *phys;
+    auto bad_arg = [&](const char* msg) {
+        // make_grid / make_rhs_context errors (grid.hpp:51-55)
+        fprintf(stderr, "hsgn_ctx_create: %s\n", msg);
+        delete c;
+        return HSGN_EINVAL;
+    };
+    if (!(grid->x_max > grid->x_min) || !(grid->y_max > grid->y_min))
+        return bad_arg("make_grid: domain extents must be increasing");
+    if (grid->nx < 4 || grid->ny < 4) return bad_arg("make_grid: need at least 4 nodes per direction");
+    if (nranks < 1 || rank < 0 || rank >= nranks || j_begin < 0 || j_end > grid->ny || j_end - j_begin < 2)
+        return bad_arg("invalid slab");
+    c->j_begin = j_begin;
+    c->j_end = j_end;
+    c->rank = rank;
+    c->nranks = nranks;
+    if (device < 0) cudaGetDevice(&device);
+    c->device = device;
+    cudaError_t e = cudaSetDevice(device);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        fprintf(stderr, "hsgn_ctx_create: %s\n", cudaGetErrorString(e));
+        delete c;
+        return HSGN_ECUDA;
+    }
+    const int ny_loc = j_end - j_begin;
+    const long long fsz = (long long)(ny_loc + 2) * grid->nx;
+    e = cudaMalloc(&c->b_alloc, sizeof(double) * fsz);
+    if (e == cudaSuccess) {
+        c->b = c->b_alloc + grid->nx;
+        e = cudaMemcpyAsync(c->b, b_host, sizeof(double) * ny_loc * grid->nx, cudaMemcpyHostToDevice, c->stream);
+    }
+    if (e == cudaSuccess) e = cudaEventCreate(&c->ev0);
+    if (e == cudaSuccess) e = cudaEventCreate(&c->ev1);
+    if (e != cudaSuccess) {
+        fprintf(stderr, "hsgn_ctx_create: %s\n", cudaGetErrorString(e));
+        hsgn_ctx_destroy(c);
+        return HSGN_ECUDA;
+    }
+    setup_ctx(c);
+    if (nranks == 1) {
+        // single slab: fill b's ghost rows for completeness (unused: wrap/clamp)
+        cudaStreamSynchronize(c->stream);
+    }
+    *out = c;
+    return HSGN_OK;
+}
+
+hsgn_status hsgn_ctx_create(const hsgn_grid* grid, const hsgn_phys* phys, const double* b_host, int device,
+                            hsgn_ctx** out) {
+    if (!grid) return HSGN_EINVAL;
+    return create_common(grid, phys, b_host, device, 0, grid->ny, 0, 1, out);
+}
+
+hsgn_status hsgn_ctx_create_slab(const hsgn_grid* grid, const hsgn_phys* phys, const double* b_host, int device,
+                                 int32_t j_begin, int32_t j_end, int32_t rank, int32_t nranks, hsgn_ctx** out) {
+    return create_common(grid, phys, b_host, device, j_begin, j_end, rank, nranks, out);
+}
+
+hsgn_status hsgn_nccl_unique_id(unsigned char out_id[128]) {
+    const NcclApi& N = nccl();
+    if (!N.ok) return HSGN_ENCCL;
+    nccl_uid id;
+    if (N.get_uid(&id)) return HSGN_ENCCL;
+    std::memcpy(out_id, id.internal, 128);
+    return HSGN_OK;
+}
+
+hsgn_status hsgn_ctx_attach_nccl(hsgn_ctx* c, const unsigned char nccl_id[128]) {
+    if (!c) return HSGN_EINVAL;
+    const NcclApi& N = nccl();
+    if (!N.ok) return fail(c, HSGN_ENCCL, "libnccl.so.2 not loadable");
+    nccl_uid id;
+    std::memcpy(id.internal, nccl_id, 128);
+    CK(cudaSetDevice(c->device));
+    int r = N.init_rank(&c->comm, c->nranks, id, c->rank);
+    if (r) return fail(c, HSGN_ENCCL, "ncclCommInitRank failed (%d)", r);
+    // exchange b's ghost rows once (static field)
+    hsgn_state bs;
+    bs.base = c->b;
+    bs.fs = c->fs;
+    hsgn_status s = exchange(c, &bs, 1);
+    if (s) return s;
+    CK(cudaStreamSynchronize(c->stream));
+    return HSGN_OK;
+}
+
+hsgn_status hsgn_ctx_destroy(hsgn_ctx* c) {
+    if (!c) return HSGN_OK;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    for (auto& kv : c->graphs)
+        if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+    if (c->ws_ready)
+        for (int k = 0; k < 8; ++k) free_state_c(c, &c->ws[k]);
+    if (c->b_alloc) cudaFree(c->b_alloc);
+    if (c->d_rec) cudaFree(c->d_rec);
+    if (c->h_rec) cudaFreeHost(c->h_rec);
+    if (c->d_halt) cudaFree(c->d_halt);
+    if (c->d_err_part) cudaFree(c->d_err_part);
+    if (c->d_scalar) cudaFree(c->d_scalar);
+    if (c->d_rows) cudaFree(c->d_rows);
+    if (c->h_rows) cudaFreeHost(c->h_rows);
+    if (c->ev0) cudaEventDestroy(c->ev0);
+    if (c->ev1) cudaEventDestroy(c->ev1);
+    if (c->comm) nccl().destroy(c->comm);
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+    return HSGN_OK;
+}
+
+const char* hsgn_last_error(const hsgn_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+hsgn_status hsgn_set_source(hsgn_ctx* c, int32_t kind) {
+    if (!c || kind < 0 || kind > 1) return HSGN_EINVAL;
+    c->source = kind;
+    return HSGN_OK;
+}
+
+hsgn_status hsgn_set_rows_per_block(hsgn_ctx* c, int32_t rows) {
+    if (!c || rows < 0) return HSGN_EINVAL;
+    c->rows_per_block = rows;
+    setup_ctx(c);
+    for (auto& kv : c->graphs)
+        if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+    c->graphs.clear();
+    if (c->ws_ready) {  // err partial buffer sized by the grid shape
+        const int need = std::max(stage_grid_blocks(c->base) + 1, wrms_blocks());
+        if (need > c->err_part_cap) {
+            cudaFree(c->d_err_part);
+            CK(cudaMalloc(&c->d_err_part, sizeof(double) * need));
+            c->err_part_cap = need;
+        }
+    }
+    return HSGN_OK;
+}
+
+int64_t hsgn_n_evals(const hsgn_ctx* c) { return c ? c->n_evals : 0; }
+
+hsgn_status hsgn_state_alloc(hsgn_ctx* c, hsgn_state** out) {
+    if (!c || !out) return HSGN_EINVAL;
+    CK(cudaSetDevice(c->device));
+    hsgn_state* s = new hsgn_state();
+    hsgn_status st = alloc_state(c, s);
+    if (st) {
+        delete s;
+        return st;
+    }
+    CK(cudaStreamSynchronize(c->stream));
+    *out = s;
+    return HSGN_OK;
+}
+
+hsgn_status hsgn_state_free(hsgn_ctx* c, hsgn_state* s) {
+    if (!c || !s) return HSGN_EINVAL;
+    cudaStreamSynchronize(c->stream);
+    free_state_c(c, s);
+    delete s;
+    return HSGN_OK;
+}
+
+hsgn_status hsgn_state_upload(hsgn_ctx* c, hsgn_state* s, const double* host) {
+    if (!c || !s || !host) return HSGN_EINVAL;
+    const long long n = (long long)c->ny_loc * c->grid.nx;
+    for (int f = 0; f < 5; ++f)
+        CK(cudaMemcpyAsync(s->f(f), host + f * n, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+    hsgn_status st = exchange(c, s, 5);
+    if (st) return st;
+    CK(cudaStreamSynchronize(c->stream));
+    return HSGN_OK;
+}
+
+hsgn_status hsgn_state_download(hsgn_ctx* c, const hsgn_state* s, double* host) {
+    if (!c || !s || !host) return HSGN_EINVAL;
+    const long long n = (long long)c->ny_loc * c->grid.nx;
+    for (int f = 0; f < 5; ++f)
+        CK(cudaMemcpyAsync(host + f * n, s->f(f), sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return HSGN_OK;
+}
+
+hsgn_status hsgn_state_copy(hsgn_ctx* c, const hsgn_state* src, hsgn_state* dst) {
+    if (!c || !src || !dst) return HSGN_EINVAL;
+    CK(cudaMemcpyAsync(dst->base - c->grid.nx, src->base - c->grid.nx, sizeof(double) * 5 * c->fs,
+                       cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return HSGN_OK;
+}
+
+hsgn_status hsgn_state_field_ptr(const hsgn_state* s, int32_t f, double** out) {
+    if (!s || !out || f < 0 || f > 4) return HSGN_EINVAL;
+    *out = s->f(f);
+    return HSGN_OK;
+}
+
+hsgn_status hsgn_rhs(hsgn_ctx* c, double t, const hsgn_state* q, hsgn_state* out, int64_t* bad_nodes) {
+    if (!c || !q || !out) return HSGN_EINVAL;
+    CK(cudaSetDevice(c->device));
+    return rhs_checked(c, t, q, out, false, bad_nodes);
+}
+
+hsgn_status hsgn_rhs_shallow_water(hsgn_ctx* c, double t, const hsgn_state* q, hsgn_state* out,
+                                   int64_t* bad_nodes) {
+    if (!c || !q || !out) return HSGN_EINVAL;
+    CK(cudaSetDevice(c->device));
+    return rhs_checked(c, t, q, out, true, bad_nodes);
+}
+
+hsgn_status hsgn_init_auxiliary(hsgn_ctx* c, hsgn_state* q) {
+    if (!c || !q) return HSGN_EINVAL;
+    CK(cudaSetDevice(c->device));
+    // u, v ghost rows must be current for the slab y-derivative
+    hsgn_status s = exchange(c, q, 3);
+    if (s) return s;
+    AuxArgs X = c->aux;
+    CK(launch_init_aux(X, q->base, c->stream));
+    s = exchange(c, q, 5);
+    if (s) return s;
+    CK(cudaStreamSynchronize(c->stream));
+    return HSGN_OK;
+}
+
+hsgn_status hsgn_total_mass(hsgn_ctx* c, const hsgn_state* q, double* out) {
+    if (!c || !q || !out) return HSGN_EINVAL;
+    return reduce_full(c, 0, q, nullptr, 0, out);
+}
+hsgn_status hsgn_total_energy(hsgn_ctx* c, const hsgn_state* q, double* out) {
+    if (!c || !q || !out) return HSGN_EINVAL;
+    return reduce_full(c, 1, q, nullptr, 0, out);
+}
+hsgn_status hsgn_energy_rate(hsgn_ctx* c, const hsgn_state* q, const hsgn_state* qt, double* out) {
+    if (!c || !q || !qt || !out) return HSGN_EINVAL;
+    return reduce_full(c, 2, q, qt, 0, out);
+}
+hsgn_status hsgn_mass_weighted_sum(hsgn_ctx* c, const hsgn_state* q, int32_t field, double* out) {
+    if (!c || !q || !out || field < 0 || field > 4) return HSGN_EINVAL;
+    return reduce_full(c, 0, q, nullptr, field, out);
+}
+hsgn_status hsgn_discrete_l2_error(hsgn_ctx* c, const hsgn_state* a, const hsgn_state* b, int32_t field,
+                                   double* out) {
+    if (!c || !a || !b || !out || field < 0 || field > 4) return HSGN_EINVAL;
+    double s2 = 0.0;
+    hsgn_status st = reduce_full(c, 3, a, b, field, &s2);
+    if (st) return st;
+    *out = std::sqrt(s2);
+    return HSGN_OK;
+}
+hsgn_status hsgn_row_sums(hsgn_ctx* c, int32_t kind, const hsgn_state* q, const hsgn_state* qt, int32_t field,
+                          double* rows_host) {
+    if (!c || !q || !rows_host || kind < 0 || kind > 3) return HSGN_EINVAL;
+    hsgn_status s = row_sums_dev(c, kind, q, qt, field);
+    if (s) return s;
+    std::memcpy(rows_host, c->h_rows, sizeof(double) * c->ny_loc);
+    return HSGN_OK;
+}
+double hsgn_outer_sum(const hsgn_grid* g, const double* rows, int32_t j_begin, int32_t j_end) {
+    return outer_sum(g, rows, j_begin, j_end);
+}
+
+hsgn_status hsgn_synchronize(hsgn_ctx* c) {
+    if (!c) return HSGN_EINVAL;
+    CK(cudaStreamSynchronize(c->stream));
+    return HSGN_OK;
+}
+
+hsgn_status hsgn_last_timing(const hsgn_ctx* c, double* ms, int64_t* kernels) {
+    if (!c) return HSGN_EINVAL;
+    if (ms) *ms = c->last_ms;
+    if (kernels) *kernels = c->last_kernels;
+    return HSGN_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------ integrator
+
+namespace {
+
+uint64_t bits_of(double v) {
+    uint64_t u;
+    std::memcpy(&u, &v, 8);
+    return u;
+}
+
+// Capture (or fetch) a graph of `steps` fused steps starting at buffer parity p.
+hsgn_status get_fixed_graph(hsgn_ctx* c, int steps, int parity, double dt, FixedGraph** out) {
+    auto key = std::make_tuple(steps, parity, 0.0, bits_of(dt), (uint64_t)c->base.rows_per_block);
+    auto it = c->graphs.find(key);
+    if (it != c->graphs.end()) {
+        *out = &it->second;
+        return HSGN_OK;
+    }
+    hsgn_state* Y[2] = {&c->ws[0], &c->ws[1]};
+    hsgn_state* K[2] = {&c->ws[2], &c->ws[3]};
+    cudaGraph_t g = nullptr;
+    CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    reset_recs(c, steps);
+    hsgn_status st = HSGN_OK;
+    for (int s = 0; s < steps && !st; ++s) {
+        const int p = (parity + s) & 1;
+        st = enqueue_step(c, Y[p], K[p], &c->ws[4], Y[p ^ 1], K[p ^ 1], nullptr, &c->d_rec[s],
+                          s ? &c->d_rec[s - 1] : nullptr, 0.0, dt, false, 0, 0, nullptr);
+    }
+    cudaError_t e = cudaStreamEndCapture(c->stream, &g);
+    if (st) {
+        if (g) cudaGraphDestroy(g);
+        return st;
+    }
+    CK(e);
+    FixedGraph fg;
+    fg.steps = steps;
+    e = cudaGraphInstantiate(&fg.exec, g, 0);
+    cudaGraphDestroy(g);
+    CK(e);
+    auto res = c->graphs.emplace(key, fg);
+    *out = &res.first->second;
+    return HSGN_OK;
+}
+
+}  // namespace
+
+// Fixed-step chunk runner: runs `steps` steps from (ws[p], ws[2+p]) without a
+// source term (graph) or with one (direct launches, t baked per step).
+// Returns the number of completed steps and the failure kind (0 none,
+// 1 depth at stage k (fail_stage), 2 floor).
+static hsgn_status run_fixed_chunk(hsgn_ctx* c, int parity, int steps, double t, double dt, int* done,
+                                   int* fail_kind, int* fail_stage, int64_t* kernels) {
+    hsgn_status st;
+    if ((st = ensure_ws(c, steps))) return st;
+    if (c->source == 0 && c->nranks == 1) {
+        FixedGraph* fg = nullptr;
+        if ((st = get_fixed_graph(c, steps, parity, dt, &fg))) return st;
+        CK(cudaGraphLaunch(fg->exec, c->stream));
+        if (kernels) *kernels += 3 * steps;
+    } else {
+        hsgn_state* Y[2] = {&c->ws[0], &c->ws[1]};
+        hsgn_state* K[2] = {&c->ws[2], &c->ws[3]};
+        reset_recs(c, steps);
+        double ts = t;
+        for (int s = 0; s < steps; ++s) {
+            const int p = (parity + s) & 1;
+            st = enqueue_step(c, Y[p], K[p], &c->ws[4], Y[p ^ 1], K[p ^ 1], nullptr, &c->d_rec[s],
+                              s ? &c->d_rec[s - 1] : nullptr, ts, dt, false, 0, 0, kernels);
+            if (st) return st;
+            ts = ts + dt;
+        }
+    }
+    CK(cudaMemcpyAsync(c->h_rec, c->d_rec, sizeof(StepRec) * steps, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    *done = steps;
+    *fail_kind = 0;
+    for (int s = 0; s < steps; ++s) {
+        const StepRec& r = c->h_rec[s];
+        for (int k = 0; k < 3; ++k)
+            if (r.bad[k]) {
+                *done = s;
+                *fail_kind = 1;
+                *fail_stage = k;
+                return HSGN_OK;
+            }
+        double mh;
+        std::memcpy(&mh, &r.minh, 8);
+        if (r.minh != ~0ull && mh <= c->phys.h_floor) {
+            *done = s;
+            *fail_kind = 2;
+            return HSGN_OK;
+        }
+    }
+    return HSGN_OK;
+}
+
+static double smin(double a, double b) { return (b < a) ? b : a; }
+static double smax(double a, double b) { return (a < b) ? b : a; }
+static double sclamp(double v, double lo, double hi) { return (v < lo) ? lo : (hi < v) ? hi : v; }
+
+// weighted_rms on device (time_integration.hpp:144-162)
+static hsgn_status wrms(hsgn_ctx* c, const hsgn_state* x, const hsgn_state* ref, double atol, double rtol,
+                        double* out) {
+    const long long n = (long long)c->ny_loc * c->grid.nx;
+    CK(launch_wrms(x->base, ref->base, atol, rtol, n, c->fs, c->d_err_part, c->stream));
+    CK(launch_sum_partials(c->d_err_part, wrms_blocks(), c->d_scalar, c->stream));
+    double s = 0;
+    CK(cudaMemcpyAsync(&s, c->d_scalar, sizeof s, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    *out = std::sqrt(s / (double)(5 * n));
+    return HSGN_OK;
+}
+
+// Depth-checked RHS into out: returns HSGN_EDEPTH (out garbage) on failure.
+static hsgn_status rhs_eval(hsgn_ctx* c, double t, const hsgn_state* q, hsgn_state* out) {
+    unsigned long long* d_bad = &c->d_rec[0].bad[0];
+    CK(cudaMemsetAsync(d_bad, 0, sizeof(unsigned long long), c->stream));
+    hsgn_status s = rhs_raw(c, t, q, out, 0.0, false, d_bad);
+    if (s) return s;
+    unsigned long long hb = 0;
+    CK(cudaMemcpyAsync(&hb, d_bad, sizeof hb, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (hb) return fail(c, HSGN_EDEPTH, "tendency evaluation at t = %f: %llu nodes with non-positive depth", t, hb);
+    return HSGN_OK;
+}
+
+extern "C" hsgn_status hsgn_solve(hsgn_ctx* c, const hsgn_state* q0, double t0, double t_final, const hsgn_cfg* cfg,
+                                  hsgn_state* q_out, hsgn_record* rec, hsgn_observer obs, void* user) {
+    if (!c || !q0 || !cfg || !q_out || !rec) return HSGN_EINVAL;
+    CK(cudaSetDevice(c->device));
+    std::memset(rec, 0, sizeof *rec);
+    rec->t = t0;
+    hsgn_status st;
+    const int CHUNK = 64;
+    if ((st = ensure_ws(c, CHUNK))) return st;
+    auto copy_state = [&](const hsgn_state* src, hsgn_state* dst) -> hsgn_status {
+        CK(cudaMemcpyAsync(dst->base - c->grid.nx, src->base - c->grid.nx, sizeof(double) * 5 * c->fs,
+                           cudaMemcpyDeviceToDevice, c->stream));
+        return HSGN_OK;
+    };
+    if ((st = copy_state(q0, q_out))) return st;
+    if (!(t_final > t0)) {
+        CK(cudaStreamSynchronize(c->stream));
+        if (t_final == t0) return HSGN_OK;
+        rec->aborted = 1;
+        snprintf(rec->reason, sizeof rec->reason, "t_final precedes t0");
+        return HSGN_OK;
+    }
+    // buffers: y = ws[p], k1 = ws[2+p], k2 = ws[4], part = ws[5], scratch ws[6], ws[7]
+    int p = 0;
+    if ((st = copy_state(q0, &c->ws[0]))) return st;
+    double t = t0;
+    auto abort_with = [&](const char* why) -> hsgn_status {
+        hsgn_status s2 = copy_state(&c->ws[p], q_out);
+        if (s2) return s2;
+        CK(cudaStreamSynchronize(c->stream));
+        rec->t = t;
+        rec->aborted = 1;
+        snprintf(rec->reason, sizeof rec->reason, "%s", why);
+        return HSGN_OK;
+    };
+    char why[256];
+    st = rhs_eval(c, t, &c->ws[0], &c->ws[2]);
+    if (st == HSGN_EDEPTH) {
+        snprintf(why, sizeof why, "initial tendency: %s", c->err.c_str());
+        return abort_with(why);
+    }
+    if (st) return st;
+    ++rec->rhs_evals;
+
+    double dt;
+    const bool fixed = cfg->fixed_dt > 0.0;
+    if (fixed)
+        dt = cfg->fixed_dt;
+    else if (cfg->dt_initial > 0.0)
+        dt = smin(cfg->dt_initial, smin(cfg->dt_max, t_final - t0));
+    else {
+        // estimate_initial_dt (time_integration.hpp:170-203)
+        const double dt_cap = smin(cfg->dt_max, t_final - t0);
+        double d0, d1;
+        if ((st = wrms(c, &c->ws[0], &c->ws[0], cfg->abs_tol, cfg->rel_tol, &d0))) return st;
+        if ((st = wrms(c, &c->ws[2], &c->ws[0], cfg->abs_tol, cfg->rel_tol, &d1))) return st;
+        if (d1 == 0.0) {
+            dt = dt_cap;
+        } else {
+            double h0 = (d0 >= 1e-5 && d1 >= 1e-5) ? 0.01 * d0 / d1 : 1e-6;
+            h0 = smin(h0, dt_cap);
+            const long long n = (long long)c->ny_loc * c->grid.nx;
+            CK(launch_axpy5(c->ws[0].base, h0, c->ws[2].base, c->ws[6].base, n, c->fs, c->stream));
+            if ((st = exchange(c, &c->ws[6], 5))) return st;
+            double d2 = 0.0;
+            bool probed = false;
+            st = rhs_eval(c, t0 + h0, &c->ws[6], &c->ws[7]);
+            if (st == HSGN_OK) {
+                ++rec->rhs_evals_setup;
+                CK(launch_axpy5(c->ws[7].base, -1.0, c->ws[2].base, c->ws[6].base, n, c->fs, c->stream));
+                double r;
+                if ((st = wrms(c, &c->ws[6], &c->ws[0], cfg->abs_tol, cfg->rel_tol, &r))) return st;
+                d2 = r / h0;
+                probed = true;
+            } else if (st != HSGN_EDEPTH) {
+                return st;
+            }
+            double h1;
+            const double dmax = smax(d1, d2);
+            if (!probed || dmax <= 1e-15)
+                h1 = smax(1e-6, h0 * 1e-3);
+            else
+                h1 = std::pow(0.01 / dmax, 1.0 / 3.0);
+            double r = 100.0 * h0;
+            if (h1 < r) r = h1;
+            if (dt_cap < r) r = dt_cap;
+            dt = r;
+        }
+        rec->rhs_evals += rec->rhs_evals_setup;
+    }
+    if (obs) {
+        CK(cudaStreamSynchronize(c->stream));
+        obs(t, &c->ws[0], &c->ws[2], user);
+    }
+
+    const double order_exp = 1.0 / 3.0;
+    double err_prev = 1.0;
+    const double tiny = 4.0 * std::numeric_limits<double>::epsilon();
+    int64_t kernels = 0;
+
+    while (t < t_final - tiny * smax(1.0, std::fabs(t_final))) {
+        if (rec->accepted + rec->rejected >= cfg->max_steps) {
+            snprintf(why, sizeof why, "step budget exhausted at t = %f", t);
+            return abort_with(why);
+        }
+        const bool clipped = dt >= t_final - t;
+        if (clipped) dt = t_final - t;
+        if (!(dt > tiny * smax(1.0, std::fabs(t)))) {
+            snprintf(why, sizeof why, "step size underflow at t = %f", t);
+            return abort_with(why);
+        }
+        if (fixed && !obs && !clipped) {
+            // plan a chunk of unclipped steps: replicate the host t sequence exactly
+            int n = 0;
+            double tt = t;
+            while (n < CHUNK && rec->accepted + rec->rejected + n < cfg->max_steps &&
+                   tt < t_final - tiny * smax(1.0, std::fabs(t_final)) && !(dt >= t_final - tt) &&
+                   (dt > tiny * smax(1.0, std::fabs(tt)))) {
+                tt = tt + dt;
+                ++n;
+            }
+            if (n >= 2) {
+                if (n & 1) --n;  // even chunks keep the buffer parity
+                int done = 0, fk = 0, fs_ = 0;
+                if ((st = run_fixed_chunk(c, p, n, t, dt, &done, &fk, &fs_, &kernels))) return st;
+                for (int s = 0; s < done; ++s) {
+                    t = t + dt;
+                    ++rec->accepted;
+                    rec->rhs_evals += 3;
+                    p ^= 1;
+                }
+                c->n_evals += 3 * (int64_t)done;
+                if (fk) {
+                    if (fk == 1) {
+                        rec->rhs_evals += fs_;
+                        c->n_evals += fs_ + 1;
+                        snprintf(why, sizeof why, "non-positive depth in fixed-step mode at t = %f", t);
+                    } else {
+                        rec->rhs_evals += 3;
+                        c->n_evals += 3;
+                        snprintf(why, sizeof why, "depth reached the floor %f during the step to t = %f",
+                                 cfg->h_floor, t + dt);
+                    }
+                    return abort_with(why);
+                }
+                continue;
+            }
+        }
+        // ---- one attempt (adaptive, clipped or observed step)
+        const int q = p ^ 1;
+        reset_recs(c, 1);
+        st = enqueue_step(c, &c->ws[p], &c->ws[2 + p], &c->ws[4], &c->ws[q], &c->ws[2 + q], &c->ws[5],
+                          &c->d_rec[0], nullptr, t, dt, !fixed, cfg->abs_tol, cfg->rel_tol, &kernels);
+        if (st) return st;
+        if (!fixed) CK(launch_sum_partials(c->d_err_part, stage_grid_blocks(c->base), c->d_scalar, c->stream));
+        StepRec r;
+        double err_sum = 0.0;
+        CK(cudaMemcpyAsync(&r, &c->d_rec[0], sizeof r, cudaMemcpyDeviceToHost, c->stream));
+        if (!fixed) CK(cudaMemcpyAsync(&err_sum, c->d_scalar, sizeof err_sum, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        int fail_stage = -1;
+        for (int k = 0; k < 3 && fail_stage < 0; ++k)
+            if (r.bad[k]) fail_stage = k;
+        c->n_evals += fail_stage < 0 ? 3 : fail_stage + 1;
+        if (fail_stage >= 0) {
+            rec->rhs_evals += fail_stage;
+            if (fixed) {
+                snprintf(why, sizeof why, "non-positive depth in fixed-step mode at t = %f", t);
+                return abort_with(why);
+            }
+            ++rec->rejected;
+            dt *= 0.25;
+            continue;
+        }
+        rec->rhs_evals += 3;
+        double err = 0.0, min_h = std::numeric_limits<double>::infinity();
+        if (r.minh != ~0ull) std::memcpy(&min_h, &r.minh, 8);
+        if (!fixed) {
+            const double n5 = 5.0 * (double)((long long)c->ny_loc * c->grid.nx);
+            err = std::sqrt(err_sum / n5);
+        }
+        const bool accept = fixed || err <= 1.0;
+        if (accept) {
+            if (min_h <= cfg->h_floor) {
+                snprintf(why, sizeof why, "depth reached the floor %f during the step to t = %f", cfg->h_floor,
+                         t + dt);
+                return abort_with(why);
+            }
+            p = q;  // swap(y, ynew); swap(k1, k4)
+            t = clipped ? t_final : t + dt;
+            ++rec->accepted;
+            if (!fixed) {
+                double fac;
+                if (err == 0.0)
+                    fac = cfg->growth_cap;
+                else
+                    fac = cfg->safety * std::pow(err, -0.7 * order_exp) * std::pow(err_prev, 0.4 * order_exp);
+                fac = sclamp(fac, cfg->shrink_floor, cfg->growth_cap);
+                dt = smin(dt * fac, cfg->dt_max);
+                err_prev = smax(err, 1e-10);
+            }
+            if (obs) obs(t, &c->ws[p], &c->ws[2 + p], user);
+        } else {
+            ++rec->rejected;
+            const double fac = std::isfinite(err) ? sclamp(cfg->safety * std::pow(err, -order_exp), 0.1, 0.9) : 0.1;
+            dt *= fac;
+        }
+    }
+    if ((st = copy_state(&c->ws[p], q_out))) return st;
+    CK(cudaStreamSynchronize(c->stream));
+    rec->t = t;
+    c->last_kernels = kernels;
+    return HSGN_OK;
+}
+
+extern "C" hsgn_status hsgn_bs3_fixed_steps(hsgn_ctx* c, hsgn_state* y, hsgn_state* k1, double t, double dt,
+                                            int64_t steps, int64_t* steps_done) {
+    if (!c || !y || !k1 || steps < 0) return HSGN_EINVAL;
+    CK(cudaSetDevice(c->device));
+    hsgn_status st;
+    const int CHUNK = 64;
+    if ((st = ensure_ws(c, CHUNK))) return st;
+    // y, k1 are caller buffers: run in the workspace pair and copy back
+    CK(cudaMemcpyAsync(c->ws[0].base - c->grid.nx, y->base - c->grid.nx, sizeof(double) * 5 * c->fs,
+                       cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->ws[2].base - c->grid.nx, k1->base - c->grid.nx, sizeof(double) * 5 * c->fs,
+                       cudaMemcpyDeviceToDevice, c->stream));
+    int p = 0;
+    int64_t done_total = 0, kernels = 0;
+    CK(cudaEventRecord(c->ev0, c->stream));
+    hsgn_status result = HSGN_OK;
+    while (done_total < steps) {
+        int n = (int)std::min<int64_t>(CHUNK, steps - done_total);
+        int done = 0, fk = 0, fs_ = 0;
+        if (n == 1) {
+            // single odd step: direct launches
+            hsgn_state* Y[2] = {&c->ws[0], &c->ws[1]};
+            hsgn_state* K[2] = {&c->ws[2], &c->ws[3]};
+            reset_recs(c, 1);
+            if ((st = enqueue_step(c, Y[p], K[p], &c->ws[4], Y[p ^ 1], K[p ^ 1], nullptr, &c->d_rec[0], nullptr, t,
+                                   dt, false, 0, 0, &kernels)))
+                return st;
+            StepRec r;
+            CK(cudaMemcpyAsync(&r, &c->d_rec[0], sizeof r, cudaMemcpyDeviceToHost, c->stream));
+            CK(cudaStreamSynchronize(c->stream));
+            done = (r.bad[0] | r.bad[1] | r.bad[2]) ? 0 : 1;
+            fk = done ? 0 : 1;
+        } else {
+            if (n & 1) --n;
+            if ((st = run_fixed_chunk(c, p, n, t, dt, &done, &fk, &fs_, &kernels))) return st;
+        }
+        for (int s = 0; s < done; ++s) {
+            t = t + dt;
+            p ^= 1;
+        }
+        done_total += done;
+        c->n_evals += 3 * (int64_t)done;
+        if (fk == 1) {
+            result = fail(c, HSGN_EDEPTH, "non-positive depth in fixed-step mode at t = %f", t);
+            break;
+        }
+    }
+    CK(cudaEventRecord(c->ev1, c->stream));
+    CK(cudaMemcpyAsync(y->base - c->grid.nx, c->ws[p].base - c->grid.nx, sizeof(double) * 5 * c->fs,
+                       cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpyAsync(k1->base - c->grid.nx, c->ws[2 + p].base - c->grid.nx, sizeof(double) * 5 * c->fs,
+                       cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c->ev0, c->ev1);
+    c->last_ms = ms;
+    c->last_kernels = kernels;
+    if (steps_done) *steps_done = done_total;
+    return result;
+}
+
+// Per-stage device time of the fused step (CUDA events around each stage
+// kernel on the context stream, averaged over `reps` steps on workspace
+// copies of (y, k1)).  ms3[k] = mean ms of stage k+1.  Used by bench.py for
+// the roofline of the dominant kernel.
+extern "C" hsgn_status hsgn_profile_stages(hsgn_ctx* c, const hsgn_state* y, const hsgn_state* k1, double dt,
+                                           int32_t reps, double* ms3) {
+    if (!c || !y || !k1 || !ms3 || reps < 1) return HSGN_EINVAL;
+    CK(cudaSetDevice(c->device));
+    hsgn_status st;
+    if ((st = ensure_ws(c, 1))) return st;
+    CK(cudaMemcpyAsync(c->ws[0].base - c->grid.nx, y->base - c->grid.nx, sizeof(double) * 5 * c->fs,
+                       cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->ws[2].base - c->grid.nx, k1->base - c->grid.nx, sizeof(double) * 5 * c->fs,
+                       cudaMemcpyDeviceToDevice, c->stream));
+    cudaEvent_t ev[4];
+    for (int k = 0; k < 4; ++k) CK(cudaEventCreate(&ev[k]));
+    double acc[3] = {0, 0, 0};
+    for (int r = 0; r < reps; ++r) {
+        reset_recs(c, 1);
+        const hsgn_state *Y = &c->ws[0], *K1 = &c->ws[2];
+        hsgn_state *K2 = &c->ws[4], *YN = &c->ws[1], *K4 = &c->ws[3];
+        StepRec* rec = &c->d_rec[0];
+        StageArgs A = stage_args(c, MODE_S1, 0.5 * dt);
+        A.a = 0.5 * dt;
+        A.y = Y->base;
+        A.k = K1->base;
+        A.out = K2->base;
+        A.bad = &rec->bad[0];
+        CK(cudaEventRecord(ev[0], c->stream));
+        if ((st = launch(c, MODE_S1, A))) return st;
+        CK(cudaEventRecord(ev[1], c->stream));
+        A = stage_args(c, MODE_S2, 0.75 * dt);
+        A.a = 0.75 * dt;
+        A.c1 = dt * (2.0 / 9.0);
+        A.c2 = dt * (1.0 / 3.0);
+        A.c3 = dt * (4.0 / 9.0);
+        A.y = Y->base;
+        A.k = K2->base;
+        A.kc = K1->base;
+        A.out = YN->base;
+        A.bad = &rec->bad[1];
+        A.minh = &rec->minh;
+        if ((st = launch(c, MODE_S2, A))) return st;
+        CK(cudaEventRecord(ev[2], c->stream));
+        A = stage_args(c, MODE_S3, dt);
+        A.y = YN->base;
+        A.out = K4->base;
+        A.bad = &rec->bad[2];
+        if ((st = launch(c, MODE_S3, A))) return st;
+        CK(cudaEventRecord(ev[3], c->stream));
+        CK(cudaEventSynchronize(ev[3]));
+        for (int k = 0; k < 3; ++k) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, ev[k], ev[k + 1]);
+            acc[k] += ms;
+        }
+    }
+    for (int k = 0; k < 4; ++k) cudaEventDestroy(ev[k]);
+    for (int k = 0; k < 3; ++k) ms3[k] = acc[k] / reps;
+    return HSGN_OK;
+}

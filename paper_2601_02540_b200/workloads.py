@@ -1,0 +1,52 @@
+"""Synthetic inputs of the BASELINE.json configurations (closed forms only).
+
+The north-star benchmark input: periodic
+[-1, 1]^2, bathymetry b = manufactured bathymetry (manufactured_generated.hpp
+:11-15), state = manufactured exact solution at t = 0.3 (:18-38), g = 9.81,
+lambda = 500, fixed dt = 0.25 dx / 20.  The closed form is restated here
+(see DESIGN.md section 5); CPU and GPU arms receive the same arrays.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from .api import BoundaryKind, make_grid
+
+
+def mms_fields(nx: int, ny: int, t: float, x_min=-1.0, x_max=1.0, y_min=-1.0, y_max=1.0,
+               kind_x=BoundaryKind.periodic, kind_y=BoundaryKind.periodic):
+    """(grid, q (5*ny*nx), b (ny*nx)) of the manufactured solution at time t."""
+    g = make_grid(x_min, x_max, y_min, y_max, nx, ny, kind_x, kind_y)
+    x = g.x(np.arange(nx))
+    y = g.y(np.arange(ny))
+    tp, fp = 2 * np.pi, 4 * np.pi
+    s1x, c1x, s2x, c2x = np.sin(tp * x), np.cos(tp * x), np.sin(fp * x), np.cos(fp * x)
+    s1y, c1y, s2y, c2y = np.sin(tp * y), np.cos(tp * y), np.sin(fp * y), np.cos(fp * y)
+    st, ct = np.sin(tp * t), np.cos(tp * t)
+    q = np.empty((5, ny, nx))
+    b = np.empty((ny, nx))
+    rows = max(1, (1 << 24) // nx)  # bounded temporaries for 8192^2
+    for j0 in range(0, ny, rows):
+        sl = slice(j0, min(ny, j0 + rows))
+        S1y, C1y, S2y, C2y = s1y[sl, None], c1y[sl, None], s2y[sl, None], c2y[sl, None]
+        bb = (2 / 25) * c1x * C1y + (1 / 25) * c2x * C2y
+        bx = -(2 / 25) * tp * s1x * C1y - (1 / 25) * fp * s2x * C2y
+        by = -(2 / 25) * tp * c1x * S1y - (1 / 25) * fp * c2x * S2y
+        h = 2 + 0.5 * s1x * S1y * ct - bb
+        u = 0.3 * s1x * st + 0 * S1y
+        v = 0.3 * S1y * st + 0 * s1x
+        ux = 0.3 * tp * c1x * st
+        vy = 0.3 * tp * C1y * st
+        b[sl] = bb
+        q[0, sl] = h
+        q[1, sl] = u
+        q[2, sl] = v
+        q[3, sl] = -h * (ux + vy) + 1.5 * (u * bx + v * by)
+        q[4, sl] = h
+    return g, q.reshape(-1), b.reshape(-1)
+
+
+def benchmark_case(n: int = 8192):
+    """Config 4 of BASELINE.json: (grid, q0, b, lambda, dt)."""
+    g, q, b = mms_fields(n, n, 0.3)
+    return g, q, b, 500.0, 0.25 * g.dx / 20.0

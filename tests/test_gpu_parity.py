@@ -1,0 +1,181 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the CPU oracle.
+
+Bar (BASELINE.json north_star): per-RHS relative error <= 1e-12; the
+kernels reproduce the reference association, so the expected and tested
+outcome is equality with `==` (IEEE equality, which identifies +0 and -0:
+the reference's y-stencil accumulates from 0.0, sbp.hpp:139-153, so only
+the sign of an exact zero may differ).  Manufactured source terms use
+device sin/cos (not correctly rounded): tolerance 1e-12 relative there.
+"""
+import numpy as np
+import pytest
+
+from oracle_lib import Oracle, Phys, default_cfg, make_grid as omake_grid, mms_exact_field, random_state
+
+pytestmark = pytest.mark.gpu
+
+import paper_2601_02540_b200 as H  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def orc():
+    return Oracle("orc")
+
+
+def hgrid(og):
+    return H.make_grid(og.x_min, og.x_max, og.y_min, og.y_max, og.nx, og.ny, og.kind_x, og.kind_y)
+
+
+def device_rhs(og, lam, b, q, t=0.0, source=False, shallow=False):
+    g = hgrid(og)
+    ctx = H.make_rhs_context(g, H.PhysSetup(9.81, lam, 1e-12, b.reshape(og.ny, og.nx)))
+    if source:
+        ctx.source = "manufactured"
+    qs = H.StateField(g, q)
+    out = H.StateField(g)
+    (H.rhs_shallow_water if shallow else H.rhs)(ctx, t, qs, out)
+    return out.flat().copy(), ctx
+
+
+def assert_equal_states(a, b, what=""):
+    a = np.asarray(a)
+    b = np.asarray(b)
+    neq = np.count_nonzero(a != b)
+    if neq:
+        idx = np.flatnonzero(a != b)[:5]
+        raise AssertionError(f"{what}: {neq} mismatches, e.g. {[(int(i), a[i], b[i]) for i in idx]}")
+
+
+CASES = [
+    # nx, ny, kind_x, kind_y, lambda
+    (64, 48, 0, 0, 500.0),
+    (257, 131, 0, 0, 500.0),
+    (33, 21, 1, 1, 500.0),
+    (40, 36, 1, 0, 500.0),
+    (36, 40, 0, 1, 30000.0),
+    (20, 18, 0, 0, 0.0),
+    (128, 128, 0, 0, 500.0),   # power-of-two spacing -> pow2 stencil path
+    (129, 65, 1, 1, 500.0),    # bounded with power-of-two 1/dx
+    (300, 7, 0, 1, 500.0),
+    (4, 4, 0, 0, 500.0),
+]
+
+
+@pytest.mark.parametrize("nx,ny,kx,ky,lam", CASES)
+def test_rhs_random_state_bitwise(orc, nx, ny, kx, ky, lam):
+    og = omake_grid(nx, ny, kind_x=kx, kind_y=ky)
+    n = nx * ny
+    q = random_state(n, 7 + nx)
+    b = 0.05 * np.sin(np.arange(n) * 0.37)
+    st, want, _ = orc.rhs(og, Phys(9.81, lam, 1e-12), b, q)
+    assert st == 0
+    got, _ = device_rhs(og, lam, b, q)
+    assert_equal_states(got, want, f"rhs {nx}x{ny} kinds=({kx},{ky}) lam={lam}")
+
+
+@pytest.mark.parametrize("nx,ny,kx,ky", [(64, 64, 0, 0), (96, 80, 1, 1), (256, 256, 0, 0), (65, 65, 1, 1)])
+def test_rhs_mms_state_bitwise(orc, nx, ny, kx, ky):
+    og = omake_grid(nx, ny, kind_x=kx, kind_y=ky)
+    q, b = mms_exact_field(og, 0.3)
+    st, want, _ = orc.rhs(og, Phys(9.81, 500.0, 1e-12), b, q)
+    got, _ = device_rhs(og, 500.0, b, q)
+    assert_equal_states(got, want, "mms state")
+
+
+def test_rhs_manufactured_source_tolerance(orc):
+    og = omake_grid(96, 96)
+    q, b = mms_exact_field(og, 0.3)
+    st, want, _ = orc.rhs(og, Phys(9.81, 500.0, 1e-12), b, q, t=0.3, source_kind=1)
+    got, _ = device_rhs(og, 500.0, b, q, t=0.3, source=True)
+    rel = np.max(np.abs(got - want)) / np.max(np.abs(want))
+    assert rel <= 1e-12, rel
+
+
+def test_rhs_shallow_water(orc):
+    og = omake_grid(48, 40)
+    n = 48 * 40
+    q = random_state(n, 31)
+    b = np.zeros(n)
+    st, want, _ = orc.rhs(og, Phys(9.81, 500.0, 1e-12), b, q, variant=1)
+    got, _ = device_rhs(og, 500.0, b, q, shallow=True)
+    assert_equal_states(got, want, "shallow water")
+    assert np.all(got[3 * n:] == 0.0)
+
+
+def test_depth_error_leaves_output_untouched():
+    og = omake_grid(8, 8)
+    g = hgrid(og)
+    ctx = H.make_rhs_context(g, H.PhysSetup(9.81, 500.0, 1e-12, np.zeros((8, 8))))
+    q = H.StateField(g)
+    q.h[:] = 1.0
+    q.eta[:] = 1.0
+    q.h[4, 3] = -0.25
+    out = H.StateField(g)
+    out.data[:] = 7.0
+    with pytest.raises(H.DepthError):
+        H.rhs(ctx, 0.0, q, out)
+    assert np.all(out.data == 7.0)
+    q.h[4, 3] = 0.0
+    with pytest.raises(H.DepthError):
+        H.rhs(ctx, 0.0, q, out)
+
+
+@pytest.mark.parametrize("nx,ny,kx,ky", [(64, 48, 0, 0), (96, 96, 1, 1), (128, 128, 0, 0), (50, 70, 1, 0)])
+def test_fixed_step_bitwise(orc, nx, ny, kx, ky):
+    og = omake_grid(nx, ny, kind_x=kx, kind_y=ky)
+    q, b = mms_exact_field(og, 0.3)
+    dx = 2.0 / nx
+    dt = 0.25 * dx / 20.0
+    cfg = default_cfg(fixed_dt=dt)
+    T = 37 * dt + 0.3 * dt  # odd number of full steps + a clipped last step
+    want, rec_w = orc.solve(og, Phys(9.81, 500.0, 1e-12), b, q, 0.0, T, cfg)
+    g = hgrid(og)
+    ctx = H.make_rhs_context(g, H.PhysSetup(9.81, 500.0, 1e-12, b.reshape(ny, nx)))
+    res = H.adaptive_solve(ctx, H.StateField(g, q), 0.0, T, H.IntegratorConfig(fixed_dt=dt))
+    assert not res.aborted and not rec_w.aborted
+    assert res.t == rec_w.t
+    assert (res.accepted, res.rejected, res.rhs_evals) == (rec_w.accepted, rec_w.rejected, rec_w.rhs_evals)
+    assert_equal_states(res.q.flat(), want, "fixed-step state")
+
+
+def test_adaptive_solve_tolerance(orc):
+    og = omake_grid(64, 64, kind_x=0, kind_y=1)
+    q, b = mms_exact_field(og, 0.3)
+    cfg = default_cfg()
+    want, rec_w = orc.solve(og, Phys(9.81, 500.0, 1e-12), b, q, 0.0, 0.01, cfg)
+    g = hgrid(og)
+    ctx = H.make_rhs_context(g, H.PhysSetup(9.81, 500.0, 1e-12, b.reshape(64, 64)))
+    res = H.adaptive_solve(ctx, H.StateField(g, q), 0.0, 0.01, H.IntegratorConfig())
+    assert not res.aborted
+    assert res.t == rec_w.t
+    assert abs(res.accepted - rec_w.accepted) <= 1
+    rel = np.max(np.abs(res.q.flat() - want)) / np.max(np.abs(want))
+    assert rel < 1e-9, rel
+
+
+def test_reductions_match_oracle(orc):
+    for kx, ky in [(0, 0), (1, 1), (1, 0)]:
+        og = omake_grid(80, 72, kind_x=kx, kind_y=ky)
+        q, b = mms_exact_field(og, 0.3)
+        ph = Phys(9.81, 500.0, 1e-12)
+        _, qt, _ = orc.rhs(og, ph, b, q)
+        g = hgrid(og)
+        ctx = H.make_rhs_context(g, H.PhysSetup(9.81, 500.0, 1e-12, b.reshape(72, 80)))
+        m = H.total_mass(ctx, H.StateField(g, q))
+        e = H.total_energy(ctx, H.StateField(g, q))
+        r = H.energy_rate(ctx, H.StateField(g, q), H.StateField(g, qt))
+        assert abs(m - orc.total_mass(og, q)) <= 1e-14 * abs(m)
+        assert abs(e - orc.total_energy(og, ph, b, q)) <= 1e-14 * abs(e)
+        assert abs(r - orc.energy_rate(og, ph, b, q, qt)) <= 1e-13 * abs(e)
+
+
+def test_init_auxiliary_bitwise(orc):
+    for kx, ky in [(0, 0), (1, 1), (0, 1)]:
+        og = omake_grid(48, 40, kind_x=kx, kind_y=ky)
+        q, b = mms_exact_field(og, 0.0)
+        want = orc.init_auxiliary(og, b, q)
+        g = hgrid(og)
+        ctx = H.make_rhs_context(g, H.PhysSetup(9.81, 500.0, 1e-12, b.reshape(40, 48)))
+        qs = H.StateField(g, q)
+        H.init_auxiliary(ctx, qs)
+        assert_equal_states(qs.flat(), want, "init_auxiliary")
