@@ -83,7 +83,7 @@ __device__ __forceinline__ void stage_input(const StageArgs& A, const Raw& r, do
 // Pointwise products of rhs.hpp:99-109.  Writes the 12 x-quantities (and the
 // centre extras when `centre`) to smem column `col` of ring slot `S`, and
 // fills the y-quantities.  Returns false when !(h > 0).
-__device__ __forceinline__ bool products(const double q[5], double b, double* S, int col,
+__device__ __forceinline__ bool products(const double q[5], double b, double* S, int col, bool store,
                                          bool centre, YQ& Y) {
     const double h = q[0], u = q[1], v = q[2], w = q[3], e = q[4];
     const bool ok = h > 0.0;
@@ -98,6 +98,7 @@ __device__ __forceinline__ bool products(const double q[5], double b, double* S,
     const double e2h = dmul(e, r);
     const double huw = dmul(hu, w);
     const double hvw = dmul(hv, w);
+    if (store) {
     S[XH * SW + col] = h;
     S[XU * SW + col] = u;
     S[XV * SW + col] = v;
@@ -113,6 +114,7 @@ __device__ __forceinline__ bool products(const double q[5], double b, double* S,
     if (centre) {
         S[CR * SW + col] = r;
         S[CRH * SW + col] = rh;
+    }
     }
     Y.h = h; Y.u = u; Y.v = v; Y.w = w; Y.e = e; Y.hhb = hhb;
     Y.v2 = v2; Y.hv = hv; Y.huv = huv; Y.e2h = e2h; Y.hvw = hvw; Y.b = b;
@@ -176,7 +178,7 @@ __device__ __forceinline__ double warp_sum(double v) {
 template <int MODE, bool POW2>
 __global__ void __launch_bounds__(BX, 3) sgn_stage_kernel(const StageArgs A) {
     extern __shared__ __align__(16) double dyn_smem[];
-    double* ring[3] = {dyn_smem, dyn_smem + NSMEM * SW, dyn_smem + 2 * NSMEM * SW};
+#define RING(k) (dyn_smem + (k) * (NSMEM * SW))
     __shared__ __align__(16) double halo_raw[2][2][11];  // [slot][left/right][fields]
     __shared__ unsigned long long s_min[BX / 32];
     __shared__ double s_err[BX / 32];
@@ -255,13 +257,13 @@ __global__ void __launch_bounds__(BX, 3) sgn_stage_kernel(const StageArgs A) {
             double q[5];
             stage_input<MODE>(A, hr, q);
             YQ unused;
-            products(q, hr.b, S, halo_scol, false, unused);
+            products(q, hr.b, S, halo_scol, true, false, unused);
         }
     };
     // S2: the part of ynew (and of the adaptive error partial) that does not
     // depend on k3 is formed when the node's raw data is in registers.
     auto centre_extras = [&](const Raw& r, double* S) {
-        if (MODE == MODE_S2) {
+        if (MODE == MODE_S2 && active) {
 #pragma unroll
             for (int f = 0; f < 5; ++f)
                 S[(CYP0 + f) * SW + tid + 1] = dadd(dadd(r.y[f], dmul(A.c1, r.kc[f])), dmul(A.c2, r.k[f]));
@@ -276,21 +278,21 @@ __global__ void __launch_bounds__(BX, 3) sgn_stage_kernel(const StageArgs A) {
         load_raw<MODE>(A, (long long)map_row(A, j0 - 1) * pitch + ic, raw);
         double q[5];
         stage_input<MODE>(A, raw, q);
-        products(q, raw.b, ring[2], tid + 1, false, yp);  // smem copy unused
+        products(q, raw.b, RING(2), tid + 1, false, false, yp);
     }
     load_raw<MODE>(A, (long long)j0 * pitch + ic, raw);
     {
         double q[5];
         stage_input<MODE>(A, raw, q);
-        const bool ok = products(q, raw.b, ring[0], tid + 1, true, yc);
+        const bool ok = products(q, raw.b, RING(0), tid + 1, active, true, yc);
         if (active && !ok) ++bad;
-        centre_extras(raw, ring[0]);
+        centre_extras(raw, RING(0));
     }
     if (j0 == 0 && clamp_lo) yp = yc;
     if (!(j0 + 1 == ny && clamp_hi)) load_raw<MODE>(A, (long long)map_row(A, j0 + 1) * pitch + ic, raw);
     if (halo_side >= 0) {
         cp_async_wait_all();
-        halo_products(0, ring[0]);
+        halo_products(0, RING(0));
         if (j0 + 1 < j1) halo_fetch(j0 + 1, 1);
     }
     int slot_cur = 0;
@@ -299,14 +301,14 @@ __global__ void __launch_bounds__(BX, 3) sgn_stage_kernel(const StageArgs A) {
     for (int j = j0; j < j1; ++j) {
         const int jn = j + 1;
         const int slot_next = slot_cur == 2 ? 0 : slot_cur + 1;
-        double* Sn = ring[slot_next];
+        double* Sn = RING(slot_next);
         const bool finish_next = jn < j1;  // will row jn be finished by this CTA?
         if (jn == ny && clamp_hi) {
             yn = yc;
         } else {
             double q[5];
             stage_input<MODE>(A, raw, q);
-            const bool ok = products(q, raw.b, Sn, tid + 1, finish_next, yn);
+            const bool ok = products(q, raw.b, Sn, tid + 1, active, finish_next, yn);
             if (active && finish_next && !ok) ++bad;
             if (finish_next) centre_extras(raw, Sn);
         }
@@ -324,7 +326,7 @@ __global__ void __launch_bounds__(BX, 3) sgn_stage_kernel(const StageArgs A) {
         __syncthreads();
 
         // ---- finish row j -------------------------------------------------
-        const double* S = ring[slot_cur];
+        const double* S = RING(slot_cur);
         if (active) {
             const double cy = ((j == 0 && clamp_lo) || (j == ny - 1 && clamp_hi)) ? A.c1y : A.cpy;
             const double h = yc.h, u = yc.u, v = yc.v, w = yc.w, b = yc.b;
