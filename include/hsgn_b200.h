@@ -109,6 +109,14 @@ hsgn_status hsgn_set_source(hsgn_ctx* ctx, int32_t kind);
 /* Launch-shape tuning (rows marched per CTA); 0 restores the default. */
 hsgn_status hsgn_set_rows_per_block(hsgn_ctx* ctx, int32_t rows);
 
+/* Stencil arithmetic variant (all bit-identical):
+ * 0 general, 1 power-of-two coefficients, 2 one common power-of-two factor
+ * (fully periodic, dx == dy).  -1 = automatic (the most specialised valid
+ * one); a request above what the grid allows is capped.  Used by the parity
+ * tests to cover every variant on the same inputs. */
+hsgn_status hsgn_set_stencil_kind(hsgn_ctx* ctx, int32_t kind);
+int32_t hsgn_stencil_kind(const hsgn_ctx* ctx);
+
 /* ctx.n_evals (rhs.hpp:28,84) */
 int64_t hsgn_n_evals(const hsgn_ctx* ctx);
 

@@ -254,6 +254,15 @@ class RhsContext:
     def set_rows_per_block(self, rows: int):
         _check(self, N.lib().hsgn_set_rows_per_block(self._h, rows), "hsgn_set_rows_per_block")
 
+    @property
+    def stencil_kind(self) -> int:
+        """0 general, 1 power-of-two, 2 common-factor (all bit-identical)."""
+        return int(N.lib().hsgn_stencil_kind(self._h))
+
+    @stencil_kind.setter
+    def stencil_kind(self, kind: int):
+        _check(self, N.lib().hsgn_set_stencil_kind(self._h, int(kind)), "hsgn_set_stencil_kind")
+
     def state(self, host=None) -> DeviceState:
         return DeviceState(self, host)
 

@@ -125,6 +125,7 @@ struct hsgn_ctx {
     AuxArgs aux{};
     int source = 0;
     int rows_per_block = 0;
+    int forced_kind = -1;  // stencil kind override (tests); -1 = automatic
     int64_t n_evals = 0;
     std::string err;
     // workspace for the integrator
@@ -229,7 +230,12 @@ static hsgn_status setup_ctx(hsgn_ctx* c) {
     A.c1y = 1.0 / c->dy;
     A.tdx = 2.0 / c->dx;
     A.tdy = 2.0 / c->dy;
-    A.pow2 = is_pow2_ge1(A.cpx) && is_pow2_ge1(A.cpy) && A.c1x == 2.0 * A.cpx && A.c1y == 2.0 * A.cpy;
+    // stencil kind (sgn_device.cuh sbp_d): 1 = power-of-two coefficients,
+    // 2 = additionally one common factor (fully periodic, dx == dy)
+    const bool p2 = is_pow2_ge1(A.cpx) && is_pow2_ge1(A.cpy) && A.c1x == 2.0 * A.cpx && A.c1y == 2.0 * A.cpy;
+    const bool cf = p2 && A.cpx == A.cpy && !A.x_bounded && A.y_lo != YE_CLAMP && A.y_hi != YE_CLAMP && !A.walls;
+    A.pow2 = cf ? 2 : (p2 ? 1 : 0);
+    if (c->forced_kind >= 0 && c->forced_kind < A.pow2) A.pow2 = c->forced_kind;
     A.g = c->phys.g;
     A.lambda = c->phys.lambda;
     A.lam_half = c->phys.lambda / 2.0;
@@ -259,7 +265,7 @@ static hsgn_status setup_ctx(hsgn_ctx* c) {
     X.x_bounded = A.x_bounded;
     X.y_bounded_lo = A.y_lo == YE_CLAMP;
     X.y_bounded_hi = A.y_hi == YE_CLAMP;
-    X.pow2 = A.pow2;
+    X.pow2 = A.pow2 >= 1;
     X.dx = c->dx;
     X.cpx = A.cpx;
     X.cpy = A.cpy;
@@ -632,14 +638,13 @@ hsgn_status hsgn_set_source(hsgn_ctx* c, int32_t kind) {
     return HSGN_OK;
 }
 
-hsgn_status hsgn_set_rows_per_block(hsgn_ctx* c, int32_t rows) {
-    if (!c || rows < 0) return HSGN_EINVAL;
-    c->rows_per_block = rows;
+static hsgn_status reconfigure(hsgn_ctx* c) {
+    cudaStreamSynchronize(c->stream);
     setup_ctx(c);
     for (auto& kv : c->graphs)
         if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
     c->graphs.clear();
-    if (c->ws_ready) {  // err partial buffer sized by the grid shape
+    if (c->d_err_part) {  // err partial buffer sized by the grid shape
         const int need = std::max(stage_grid_blocks(c->base) + 1, wrms_blocks());
         if (need > c->err_part_cap) {
             cudaFree(c->d_err_part);
@@ -649,6 +654,20 @@ hsgn_status hsgn_set_rows_per_block(hsgn_ctx* c, int32_t rows) {
     }
     return HSGN_OK;
 }
+
+hsgn_status hsgn_set_rows_per_block(hsgn_ctx* c, int32_t rows) {
+    if (!c || rows < 0) return HSGN_EINVAL;
+    c->rows_per_block = rows;
+    return reconfigure(c);
+}
+
+hsgn_status hsgn_set_stencil_kind(hsgn_ctx* c, int32_t kind) {
+    if (!c || kind < -1 || kind > 2) return HSGN_EINVAL;
+    c->forced_kind = kind;
+    return reconfigure(c);
+}
+
+int32_t hsgn_stencil_kind(const hsgn_ctx* c) { return c ? c->base.pow2 : -1; }
 
 int64_t hsgn_n_evals(const hsgn_ctx* c) { return c ? c->n_evals : 0; }
 

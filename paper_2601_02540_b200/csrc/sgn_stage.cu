@@ -8,15 +8,21 @@
 // point) and epilogue (ynew in stage 2, error partials in adaptive mode).
 //
 // Work decomposition:
-//   * a CTA owns a BX-column tile and marches down a strip of rows;
-//   * each thread owns one column: stage inputs of the NEXT row are loaded
-//     into registers one row ahead (software pipelining), pointwise products
-//     are formed once per node and parked in a 3-row shared-memory ring
-//     (x-neighbours are read from there), while the y-neighbours live in a
-//     register rolling window (prev / next row of the 12 y-quantities);
-//   * the two halo columns of the tile are fetched with cp.async (LDGSTS)
-//     straight into shared memory one row ahead, so no register is spent on
-//     them;
+//   * a CTA of BX = 128 threads owns BX consecutive columns, i.e. BX-2
+//     finished columns plus the left/right halo column (overlapped tiles:
+//     every thread does identical product work, the two edge threads skip
+//     the combine, so no warp is ever late at the per-row barrier);
+//   * the CTA marches down a strip of rows; each thread loads the raw
+//     inputs of the NEXT row into registers one row ahead (software
+//     pipelining);
+//   * the y-stencil uses a register window: the 12 y-differentiated
+//     quantities of rows j-1 and j+1 (three named sets whose roles rotate
+//     with the 3x-unrolled march, so no register moves);
+//   * the x-stencil reads columns i-1, i+1 of a 3-row shared-memory ring
+//     that holds only the node's stage inputs and two derived scalars (four
+//     16-byte double2 pairs); the neighbours' products are re-formed from
+//     them with the identical operations, which costs less than moving them
+//     (the kernel is bound by the shared-memory pipe, ncu r1c);
 //   * bounded (wall) directions use the same arithmetic form with clamped
 //     neighbours and the closure coefficient 1/dx (see sbp_d), plus the SAT
 //     face term; periodic x wraps by index, periodic y wraps or reads ghost
@@ -29,26 +35,39 @@
 
 namespace hsgn_dev {
 
-constexpr int BX = 128;   // columns per CTA tile == threads per CTA
-constexpr int SW = BX + 2;  // smem row width incl. 2 halo columns
+constexpr int BX = 128;     // threads per CTA == columns touched per tile
+constexpr int WX = BX - 2;  // finished columns per tile
+#ifndef HSGN_MIN_BLOCKS
+#define HSGN_MIN_BLOCKS 3
+#endif
 
-struct Raw {              // raw stage-input data at one node
+template <int MODE>
+__host__ __device__ constexpr int npairs() { return MODE == MODE_S2 ? NPAIRS_S2 : NPAIRS; }
+template <int MODE>
+__host__ __device__ constexpr int min_blocks() { return HSGN_MIN_BLOCKS; }
+
+// Per-field device pointers (kernel parameters live in the constant bank, so
+// every global address is one IMAD.WIDE of the 32-bit node offset).
+struct KPtrs {
+    const double* y[5];
+    const double* k[5];
+    const double* kc[5];
+    const double* b;
+    double* out[5];
+    double* part[5];
+    const double* yold[5];
+};
+
+struct Raw {  // raw stage-input data at one node
     double y[5];
     double k[5];
-    double kc[5];         // S2 only: k1 (for the fused ynew)
+    double kc[5];  // S2 only: k1 (for the fused ynew)
     double b;
 };
 
-struct YQ {               // y-differentiated quantities at one node (rhs.hpp:127-137 + b)
+struct YQ {  // y-differentiated quantities of one row at this column (rhs.hpp:127-137 + b)
     double h, u, v, w, e, hhb, v2, hv, huv, e2h, hvw, b;
 };
-
-__device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
-    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
 // Memory row index of logical row jr (may be -1 or ny) of the slab.
 __device__ __forceinline__ int map_row(const StageArgs& A, int jr) {
@@ -58,72 +77,69 @@ __device__ __forceinline__ int map_row(const StageArgs& A, int jr) {
 }
 
 template <int MODE>
-__device__ __forceinline__ void load_raw(const StageArgs& A, long long off, Raw& r) {
+__device__ __forceinline__ void load_raw(const KPtrs& P, unsigned off, Raw& r) {
 #pragma unroll
-    for (int f = 0; f < 5; ++f) r.y[f] = __ldg(A.y + f * A.fs + off);
+    for (int f = 0; f < 5; ++f) r.y[f] = __ldg(P.y[f] + off);
     if (MODE == MODE_S1 || MODE == MODE_S2) {
 #pragma unroll
-        for (int f = 0; f < 5; ++f) r.k[f] = __ldg(A.k + f * A.fs + off);
+        for (int f = 0; f < 5; ++f) r.k[f] = __ldg(P.k[f] + off);
     }
     if (MODE == MODE_S2) {
 #pragma unroll
-        for (int f = 0; f < 5; ++f) r.kc[f] = __ldg(A.kc + f * A.fs + off);
+        for (int f = 0; f < 5; ++f) r.kc[f] = __ldg(P.kc[f] + off);
     }
-    r.b = __ldg(A.b + off);
+    r.b = __ldg(P.b + off);
 }
 
-// Stage input q = y + a*k (state_add1, time_integration.hpp:61-75).
+// Pointwise products of rhs.hpp:99-109 at one node, from the stage input
+// q = y + a*k (state_add1, time_integration.hpp:61-75).  Stores the ring
+// pairs of the node (S already offset by ring row and column), fills the
+// y-quantities; returns h > 0.
 template <int MODE>
-__device__ __forceinline__ void stage_input(const StageArgs& A, const Raw& r, double q[5]) {
+__device__ __forceinline__ bool products(const StageArgs& A, const Raw& raw, double2* S, YQ& Y) {
+    double q[5];
 #pragma unroll
     for (int f = 0; f < 5; ++f)
-        q[f] = (MODE == MODE_S1 || MODE == MODE_S2) ? dadd(r.y[f], dmul(A.a, r.k[f])) : r.y[f];
-}
-
-// Pointwise products of rhs.hpp:99-109.  Writes the 12 x-quantities (and the
-// centre extras when `centre`) to smem column `col` of ring slot `S`, and
-// fills the y-quantities.  Returns false when !(h > 0).
-__device__ __forceinline__ bool products(const double q[5], double b, double* S, int col, bool store,
-                                         bool centre, YQ& Y) {
-    const double h = q[0], u = q[1], v = q[2], w = q[3], e = q[4];
+        q[f] = (MODE == MODE_S1 || MODE == MODE_S2) ? dadd(raw.y[f], dmul(A.a, raw.k[f])) : raw.y[f];
+    const double h = q[0], u = q[1], v = q[2], w = q[3], e = q[4], b = raw.b;
     const bool ok = h > 0.0;
     const double rh = __drcp_rn(h);
-    const double r = div_by(e, h, rh);
-    const double hu = dmul(h, u);
+    bool slow = false;
+    double r = div_fast(e, h, rh, slow);  // eta/h computed once (rhs.hpp:86-88)
+    if (slow) r = e / h;
+    const double hpb = dadd(h, b);
     const double hv = dmul(h, v);
-    const double huv = dmul(hu, v);  // (h*u)*v
-    const double u2 = dmul(u, u);
-    const double v2 = dmul(v, v);
-    const double hhb = dmul(h, dadd(h, b));
-    const double e2h = dmul(e, r);
-    const double huw = dmul(hu, w);
-    const double hvw = dmul(hv, w);
-    if (store) {
-    S[XH * SW + col] = h;
-    S[XU * SW + col] = u;
-    S[XV * SW + col] = v;
-    S[XW * SW + col] = w;
-    S[XE * SW + col] = e;
-    S[XHHB * SW + col] = hhb;
-    S[XU2 * SW + col] = u2;
-    S[XHU * SW + col] = hu;
-    S[XHUV * SW + col] = huv;
-    S[XE2H * SW + col] = e2h;
-    S[XHUW * SW + col] = huw;
-    S[XB * SW + col] = b;
-    if (centre) {
-        S[CR * SW + col] = r;
-        S[CRH * SW + col] = rh;
+    S[P_HU * BX] = make_double2(h, u);
+    S[P_VW * BX] = make_double2(v, w);
+    S[P_EB * BX] = make_double2(e, b);
+    S[P_RHB * BX] = make_double2(r, hpb);
+    S[P_RH * BX] = make_double2(rh, 0.0);
+    if (MODE == MODE_S2) {  // ((y + c1 k1) + c2 k2): the k3-free part of ynew (state_add3)
+        double yp[5];
+#pragma unroll
+        for (int f = 0; f < 5; ++f) yp[f] = dadd(dadd(raw.y[f], dmul(A.c1, raw.kc[f])), dmul(A.c2, raw.k[f]));
+        S[P_YP01 * BX] = make_double2(yp[0], yp[1]);
+        S[P_YP23 * BX] = make_double2(yp[2], yp[3]);
+        S[P_YP4 * BX] = make_double2(yp[4], 0.0);
     }
-    }
-    Y.h = h; Y.u = u; Y.v = v; Y.w = w; Y.e = e; Y.hhb = hhb;
-    Y.v2 = v2; Y.hv = hv; Y.huv = huv; Y.e2h = e2h; Y.hvw = hvw; Y.b = b;
+    Y.h = h;
+    Y.u = u;
+    Y.v = v;
+    Y.w = w;
+    Y.e = e;
+    Y.b = b;
+    Y.hhb = dmul(h, hpb);
+    Y.v2 = dmul(v, v);
+    Y.hv = hv;
+    Y.huv = dmul(dmul(h, u), v);  // (h*u)*v
+    Y.e2h = dmul(e, r);
+    Y.hvw = dmul(hv, w);
     return ok;
 }
 
 // Manufactured source terms S(t, x, y) (scenarios.hpp:179-217 forcing; the
 // closed form restated in DESIGN.md section 5 and oracle/hsgn_oracle.c).
-__device__ void mms_source(double t, double x, double y, double g, double s[5]) {
+__device__ __noinline__ void mms_source(double t, double x, double y, double g, double* s) {
     const double tp = 2.0 * 3.14159265358979323846, fp = 4.0 * 3.14159265358979323846;
     double s1x, c1x, s1y, c1y, s2x, c2x, s2y, c2y, st, ct;
     sincos(tp * x, &s1x, &c1x);
@@ -160,6 +176,40 @@ __device__ void mms_source(double t, double x, double y, double g, double s[5]) 
     s[4] = sh;
 }
 
+// Adaptive-mode epilogues, kept out of line so they do not raise the register
+// pressure of the fixed-step kernels.  (Scalars and base pointers are passed
+// by value: taking the address of the kernel-parameter structs would copy
+// them to local memory.)
+// S2: ((d1 k1 + d2 k2) + d3 k3) (time_integration.hpp:128-129, first 3 terms)
+__device__ __noinline__ void s2_error_partial(const double* kc, const double* k, double* part, long long fs,
+                                              unsigned off, double d1, double d2, double d3, double o0, double o1,
+                                              double o2, double o3, double o4) {
+    const double o[5] = {o0, o1, o2, o3, o4};
+#pragma unroll
+    for (int f = 0; f < 5; ++f) {
+        const double k1v = __ldg(kc + f * fs + off);
+        const double k2v = __ldg(k + f * fs + off);
+        part[f * fs + off] = dadd(dadd(dmul(d1, k1v), dmul(d2, k2v)), dmul(d3, o[f]));
+    }
+}
+// S3: sum_f (e_f / scale_f)^2 at one node (time_integration.hpp:127-136)
+__device__ __noinline__ double s3_error_sq(const double* part, const double* yold, const double* ynew, long long fs,
+                                           unsigned off, double dt, double d4, double atol, double rtol, double o0,
+                                           double o1, double o2, double o3, double o4) {
+    const double o[5] = {o0, o1, o2, o3, o4};
+    double acc = 0.0;
+#pragma unroll
+    for (int f = 0; f < 5; ++f) {
+        const double e = dmul(dt, dadd(part[f * fs + off], dmul(d4, o[f])));
+        const double ay = fabs(__ldg(yold + f * fs + off));
+        const double an = fabs(__ldg(ynew + f * fs + off));
+        const double scale = dadd(atol, dmul(rtol, ay < an ? an : ay));
+        const double rq = e / scale;
+        acc = dadd(acc, dmul(rq, rq));
+    }
+    return acc;
+}
+
 __device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -175,11 +225,188 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
-template <int MODE, bool POW2>
-__global__ void __launch_bounds__(BX, 3) sgn_stage_kernel(const StageArgs A) {
-    extern __shared__ __align__(16) double dyn_smem[];
-#define RING(k) (dyn_smem + (k) * (NSMEM * SW))
-    __shared__ __align__(16) double halo_raw[2][2][11];  // [slot][left/right][fields]
+// Per-thread constants and accumulators of one CTA's march.
+struct Thr {
+    int tid, i, j1;
+    bool finish, xl, xr;
+    unsigned col;       // memory column this thread loads (wrapped / clamped)
+    double cx;          // x-stencil coefficient of this column
+    int sl, sr;         // ring columns of aL / aR
+    int jc0, jc1;       // rows that use the y closure coefficient (clamped walls)
+    unsigned long long bad, my_min;
+    double my_err;
+};
+
+// x-quantities of a neighbour column re-formed from its ring pairs, with the
+// operations of products() / rhs.hpp:99-109 (bit-identical).
+struct XQ {
+    double h, u, v, w, e, b, hhb, u2, hu, huv, e2h, huw;
+};
+__device__ __forceinline__ void neighbour_x(const double2* S, XQ& X) {
+    const double2 p0 = S[P_HU * BX], p1 = S[P_VW * BX], p2 = S[P_EB * BX], p3 = S[P_RHB * BX];
+    X.h = p0.x;
+    X.u = p0.y;
+    X.v = p1.x;
+    X.w = p1.y;
+    X.e = p2.x;
+    X.b = p2.y;
+    X.hhb = dmul(X.h, p3.y);
+    X.u2 = dmul(X.u, X.u);
+    X.hu = dmul(X.h, X.u);
+    X.huv = dmul(X.hu, X.v);
+    X.e2h = dmul(X.e, p3.x);
+    X.huw = dmul(X.hu, X.w);
+}
+
+// One row of the march: form row jn = j+1 (ring slot SN, register set yn),
+// then finish row j (ring slot SC; row j-1 is register set yp).
+template <int MODE, int KIND, int SC>
+__device__ __forceinline__ void march_row(const StageArgs& A, const KPtrs& P, Thr& T, double2* ring, int j,
+                                          const YQ& yp, YQ& yn, Raw& raw) {
+    constexpr int NP = npairs<MODE>();
+    constexpr int SN = (SC + 1) % 3;
+    const int jn = j + 1;
+    const unsigned nx = (unsigned)A.nx;
+    {  // products of row jn (for D_y of row j, and D_x of row jn one step later)
+        const bool ok = products<MODE>(A, raw, ring + SN * (NP * BX) + T.tid, yn);
+        if (T.finish && jn < T.j1 && !ok) ++T.bad;
+    }
+    // software pipelining: raw inputs of row jn+1 are in flight during the finish
+    if (jn < T.j1) load_raw<MODE>(P, (unsigned)map_row(A, jn + 1) * nx + T.col, raw);
+    // One barrier per row: row j's ring entries (written one step ago) become
+    // visible, and this step's writes to slot SN are ordered after the last
+    // reads of that slot (finish of row j-2, before the previous barrier).
+    __syncthreads();
+    if (!T.finish) return;
+
+    const double2* S = ring + SC * (NP * BX);
+    const double2* Sc = S + T.tid;  // row j, own column
+    const double cx = T.cx;
+    const double cy = (j == T.jc0 || j == T.jc1) ? A.c1y : A.cpy;
+    // centre values of row j (products re-formed as in rhs.hpp:99-109)
+    const double2 c0 = Sc[P_HU * BX], c1 = Sc[P_VW * BX], c2 = Sc[P_EB * BX], c3 = Sc[P_RHB * BX];
+    const double h = c0.x, u = c0.y, v = c1.x, w = c1.y, b = c2.y, r = c3.x, hpb = c3.y;
+    const double rh = Sc[P_RH * BX].x;
+    const double hu = dmul(h, u), u2 = dmul(u, u), hv = dmul(h, v), v2 = dmul(v, v);
+    // x-neighbours i-1, i+1
+    XQ L, R;
+    neighbour_x(S + T.sl, L);
+    neighbour_x(S + T.sr, R);
+#define DX(f) const double d##f##_x = sbp_d<KIND>(cx, L.f, R.f)
+#define DY(f) const double d##f##_y = sbp_d<KIND>(cy, yp.f, yn.f)
+    DX(h); DX(u); DX(v); DX(w); DX(e); DX(b); DX(hhb); DX(u2); DX(hu); DX(huv); DX(e2h); DX(huw);
+    DY(h); DY(u); DY(v); DY(w); DY(e); DY(b); DY(hhb); DY(v2); DY(hv); DY(huv); DY(e2h); DY(hvw);
+#undef DX
+#undef DY
+    const double g = A.g;
+    // KIND 2: every tendency sum is linear in the (undivided) differences, so
+    // the stencil coefficient is applied once per tendency (exact: power of 2)
+    auto sc = [&](double x) { return KIND == 2 ? dmul(A.cpx, x) : x; };
+    // s + 0.5*G as one rounding: 0.5*G is exact, so fma(0.5, G, s) == RN(s + RN(0.5 G))
+    auto add_half = [](double s, double G) { return __fma_rn(0.5, G, s); };
+    double o[5];
+    {  // continuity (rhs.hpp:156-157) + wall SAT (sbp.hpp:272-284)
+        const double s = sc(dadd(dadd(dadd(dmul(u, dh_x), dmul(h, du_x)), dmul(v, dh_y)), dmul(h, dv_y)));
+        double ht = -s;
+        if (A.walls) {
+            double sat = 0.0;
+            if (T.xl) sat = dsub(sat, dmul(A.tdx, hu));
+            if (T.xr) sat = dadd(sat, dmul(A.tdx, hu));
+            if (j == 0 && A.sat_y_lo) sat = dsub(sat, dmul(A.tdy, hv));
+            if (j == A.ny - 1 && A.sat_y_hi) sat = dadd(sat, dmul(A.tdy, hv));
+            ht = dadd(ht, sat);
+        }
+        o[0] = ht;
+    }
+    const double ghb = dmul(g, hpb);
+    const double ls_rr = dmul(A.lam_sixth, dmul(r, r));
+    const double lt_r = dmul(A.lam_third, r);
+    const double omr = dsub(1.0, r);
+    const double lh_omr = dmul(A.lam_half, omr);
+    const double uv = dmul(u, v);
+    double nu, nv, nw;  // division numerators (before the common factor in KIND 2)
+    {  // x-momentum (rhs.hpp:167-175), 0.5 factored out of the two split groups
+        double s = dsub(dmul(g, dhhb_x), dmul(ghb, dh_x));
+        s = add_half(s, dsub(dadd(dsub(dmul(h, du2_x), dmul(u2, dh_x)), dmul(u, dhu_x)), dmul(hu, du_x)));
+        s = add_half(s, dsub(dadd(dsub(dhuv_y, dmul(uv, dh_y)), dmul(hv, du_y)), dmul(hu, dv_y)));
+        s = dadd(s, dadd(dsub(dsub(dadd(dmul(ls_rr, dh_x), dmul(A.lam_third, de_x)), dmul(lt_r, de_x)),
+                              dmul(A.lam_sixth, de2h_x)),
+                         dmul(lh_omr, db_x)));
+        nu = -s;
+    }
+    {  // y-momentum (rhs.hpp:180-188)
+        double s = dsub(dmul(g, dhhb_y), dmul(ghb, dh_y));
+        s = add_half(s, dsub(dadd(dsub(dmul(h, dv2_y), dmul(v2, dh_y)), dmul(v, dhv_y)), dmul(hv, dv_y)));
+        s = add_half(s, dsub(dadd(dsub(dhuv_x, dmul(uv, dh_x)), dmul(hu, dv_x)), dmul(hv, du_x)));
+        s = dadd(s, dadd(dsub(dsub(dadd(dmul(ls_rr, dh_y), dmul(A.lam_third, de_y)), dmul(lt_r, de_y)),
+                              dmul(A.lam_sixth, de2h_y)),
+                         dmul(lh_omr, db_y)));
+        nv = -s;
+    }
+    {  // vertical velocity (rhs.hpp:196-200)
+        const double hw = dmul(h, w);
+        double s = dmul(0.5, dsub(dsub(dadd(dhuw_x, dmul(hu, dw_x)), dmul(dmul(u, w), dh_x)), dmul(hw, du_x)));
+        s = add_half(s, dsub(dsub(dadd(dhvw_y, dmul(hv, dw_y)), dmul(dmul(v, w), dh_y)), dmul(hw, dv_y)));
+        nw = dsub(dmul(A.lambda, omr), sc(s));
+    }
+    {  // the three "/h" (rhs.hpp:175,188,200), one range test per node
+        bool slow = false;
+        double qu = div_fast(nu, h, rh, slow), qv = div_fast(nv, h, rh, slow), qw = div_fast(nw, h, rh, slow);
+        if (slow) {
+            qu = nu / h;
+            qv = nv / h;
+            qw = nw / h;
+        }
+        o[1] = sc(qu);  // RN(c s / h) == c RN(s / h) for c a power of two
+        o[2] = sc(qv);
+        o[3] = qw;
+    }
+    {  // auxiliary depth (rhs.hpp:206-208)
+        const double s =
+            dadd(dadd(dadd(dmul(u, de_x), dmul(v, de_y)), dmul(dmul(1.5, u), db_x)), dmul(dmul(1.5, v), db_y));
+        o[4] = dsub(w, sc(s));
+    }
+    if (A.shallow) {  // rhs_shallow_water zeroes the decoupled tendencies
+        o[3] = 0.0;
+        o[4] = 0.0;
+    }
+    if (A.source) {  // add_manufactured_sources: after assembly (rhs.hpp:212-213)
+        const double xg = dadd(A.x_min, dmul((double)T.i, A.dx));
+        const double yg = dadd(A.y_min, dmul((double)(A.j_global0 + j), A.dy));
+        double s5[5];
+        mms_source(A.t, xg, yg, A.g, s5);
+#pragma unroll
+        for (int f = 0; f < 5; ++f) o[f] = dadd(o[f], s5[f]);
+    }
+    // ---- epilogue
+    const unsigned off = (unsigned)j * nx + T.col;
+    if (MODE == MODE_S2) {
+        const double2 y01 = Sc[P_YP01 * BX], y23 = Sc[P_YP23 * BX], y4 = Sc[P_YP4 * BX];
+        const double ypart[5] = {y01.x, y01.y, y23.x, y23.y, y4.x};
+#pragma unroll
+        for (int f = 0; f < 5; ++f) {  // state_add3: ((y + c1 k1) + c2 k2) + c3 k3
+            const double yn_f = dadd(ypart[f], dmul(A.c3, o[f]));
+            P.out[f][off] = yn_f;
+            if (f == 0) {
+                const unsigned long long bits = (unsigned long long)__double_as_longlong(yn_f);
+                T.my_min = bits < T.my_min ? bits : T.my_min;
+            }
+        }
+        if (A.adaptive)
+            s2_error_partial(A.kc, A.k, A.part, A.fs, off, A.d1, A.d2, A.d3, o[0], o[1], o[2], o[3], o[4]);
+    } else {
+#pragma unroll
+        for (int f = 0; f < 5; ++f) P.out[f][off] = o[f];
+        if (MODE == MODE_S3 && A.adaptive)
+            T.my_err = dadd(T.my_err, s3_error_sq(A.part, A.yold, A.y, A.fs, off, A.dt, A.d4, A.atol, A.rtol, o[0],
+                                                  o[1], o[2], o[3], o[4]));
+    }
+}
+
+template <int MODE, int KIND>
+__global__ void __launch_bounds__(BX, min_blocks<MODE>()) sgn_stage_kernel(const StageArgs A, const KPtrs P) {
+    constexpr int NP = npairs<MODE>();
+    extern __shared__ __align__(16) double2 ring[];  // 3 x NP x BX pairs
     __shared__ unsigned long long s_min[BX / 32];
     __shared__ double s_err[BX / 32];
     __shared__ int s_skip;
@@ -203,271 +430,57 @@ __global__ void __launch_bounds__(BX, 3) sgn_stage_kernel(const StageArgs A) {
     }
 
     const int nx = A.nx, ny = A.ny;
-    const int i0 = blockIdx.x * BX;
-    const int i = i0 + tid;
-    const bool active = i < nx;
-    const int ic = active ? i : nx - 1;  // idle lanes load a valid column
-    const int width = min(BX, nx - i0);
+    Thr T;
+    T.tid = tid;
+    const int i = (int)blockIdx.x * WX - 1 + tid;  // logical column (may be -1 or >= nx)
+    T.i = i;
+    T.finish = tid >= 1 && tid <= WX && i < nx;
+    // memory column: periodic wrap of the two halo columns, clamp otherwise
+    int col = i;
+    if (i < 0) col = A.x_bounded ? 0 : nx - 1;
+    if (i >= nx) col = (A.x_bounded || i > nx) ? nx - 1 : 0;
+    T.col = (unsigned)col;
+    T.xl = A.x_bounded && i == 0;
+    T.xr = A.x_bounded && i == nx - 1;
+    T.cx = (T.xl || T.xr) ? A.c1x : A.cpx;
+    T.sl = T.xl ? tid : tid - 1;
+    T.sr = T.xr ? tid : tid + 1;
     const int j0 = blockIdx.y * A.rows_per_block;
-    const int j1 = min(ny, j0 + A.rows_per_block);
-    const long long pitch = nx;
+    T.j1 = min(ny, j0 + A.rows_per_block);
+    T.jc0 = A.y_lo == YE_CLAMP ? 0 : -2;
+    T.jc1 = A.y_hi == YE_CLAMP ? ny - 1 : -2;
+    T.bad = 0;
+    T.my_min = ~0ull;
+    T.my_err = 0.0;
+    const unsigned unx = (unsigned)nx;
 
-    // x-stencil of this column: interior, or the clamped SBP closure row
-    const bool xl = A.x_bounded && i == 0;
-    const bool xr = A.x_bounded && i == nx - 1;
-    const double cx = (xl || xr) ? A.c1x : A.cpx;
-    const int sl = xl ? tid + 1 : tid;      // smem column of aL
-    const int sr = xr ? tid + 1 : tid + 2;  // smem column of aR
-    // halo columns of the tile: thread 0 -> left (smem col 0), thread 32 -> right
-    const int halo_side = (tid == 0) ? 0 : ((tid == 32) ? 1 : -1);
-    const bool halo_live = halo_side == 0 ? (i0 > 0 || !A.x_bounded)
-                                          : (halo_side == 1 ? (i0 + width < nx || !A.x_bounded) : false);
-    const int halo_i = halo_side == 0 ? (i0 > 0 ? i0 - 1 : nx - 1) : (i0 + width < nx ? i0 + width : 0);
-    const int halo_scol = halo_side == 0 ? 0 : width + 1;
-    const bool clamp_lo = A.y_lo == YE_CLAMP, clamp_hi = A.y_hi == YE_CLAMP;
-
-    unsigned long long bad = 0;
-    unsigned long long my_min = ~0ull;
-    double my_err = 0.0;
-
-    auto halo_fetch = [&](int jr, int hs) {  // async copy of the halo node's raw inputs
-        if (halo_live) {
-            const long long off = (long long)map_row(A, jr) * pitch + halo_i;
-            double* d = halo_raw[hs][halo_side];
-#pragma unroll
-            for (int f = 0; f < 5; ++f) cp_async8(d + f, A.y + f * A.fs + off);
-            if (MODE == MODE_S1 || MODE == MODE_S2) {
-#pragma unroll
-                for (int f = 0; f < 5; ++f) cp_async8(d + 5 + f, A.k + f * A.fs + off);
-            }
-            cp_async8(d + 10, A.b + off);
-        }
-        cp_async_commit();
-    };
-    auto halo_products = [&](int hs, double* S) {
-        if (halo_live) {
-            const double* d = halo_raw[hs][halo_side];
-            Raw hr;
-#pragma unroll
-            for (int f = 0; f < 5; ++f) {
-                hr.y[f] = d[f];
-                hr.k[f] = d[5 + f];
-            }
-            hr.b = d[10];
-            double q[5];
-            stage_input<MODE>(A, hr, q);
-            YQ unused;
-            products(q, hr.b, S, halo_scol, true, false, unused);
-        }
-    };
-    // S2: the part of ynew (and of the adaptive error partial) that does not
-    // depend on k3 is formed when the node's raw data is in registers.
-    auto centre_extras = [&](const Raw& r, double* S) {
-        if (MODE == MODE_S2 && active) {
-#pragma unroll
-            for (int f = 0; f < 5; ++f)
-                S[(CYP0 + f) * SW + tid + 1] = dadd(dadd(r.y[f], dmul(A.c1, r.kc[f])), dmul(A.c2, r.k[f]));
-        }
-    };
-
-    // ---- prologue: rows j0-1 (prev, y-quantities only) and j0 (cur) ----------
-    YQ yp, yc, yn;
+    // ---- prologue: row j0-1 -> register set C (ring slot 2), row j0 -> set A (slot 0)
+    YQ ya, yb, yc;
     Raw raw;
-    if (halo_side >= 0) halo_fetch(j0, 0);
-    if (!(j0 == 0 && clamp_lo)) {
-        load_raw<MODE>(A, (long long)map_row(A, j0 - 1) * pitch + ic, raw);
-        double q[5];
-        stage_input<MODE>(A, raw, q);
-        products(q, raw.b, RING(2), tid + 1, false, false, yp);
-    }
-    load_raw<MODE>(A, (long long)j0 * pitch + ic, raw);
+    load_raw<MODE>(P, (unsigned)map_row(A, j0 - 1) * unx + T.col, raw);
+    products<MODE>(A, raw, ring + 2 * (NP * BX) + tid, yc);
+    load_raw<MODE>(P, (unsigned)j0 * unx + T.col, raw);
     {
-        double q[5];
-        stage_input<MODE>(A, raw, q);
-        const bool ok = products(q, raw.b, RING(0), tid + 1, active, true, yc);
-        if (active && !ok) ++bad;
-        centre_extras(raw, RING(0));
+        const bool ok = products<MODE>(A, raw, ring + tid, ya);
+        if (T.finish && !ok) ++T.bad;
     }
-    if (j0 == 0 && clamp_lo) yp = yc;
-    if (!(j0 + 1 == ny && clamp_hi)) load_raw<MODE>(A, (long long)map_row(A, j0 + 1) * pitch + ic, raw);
-    if (halo_side >= 0) {
-        cp_async_wait_all();
-        halo_products(0, RING(0));
-        if (j0 + 1 < j1) halo_fetch(j0 + 1, 1);
-    }
-    int slot_cur = 0;
+    load_raw<MODE>(P, (unsigned)map_row(A, j0 + 1) * unx + T.col, raw);
 
-    // ---- march down the strip --------------------------------------------
-    for (int j = j0; j < j1; ++j) {
-        const int jn = j + 1;
-        const int slot_next = slot_cur == 2 ? 0 : slot_cur + 1;
-        double* Sn = RING(slot_next);
-        const bool finish_next = jn < j1;  // will row jn be finished by this CTA?
-        if (jn == ny && clamp_hi) {
-            yn = yc;
-        } else {
-            double q[5];
-            stage_input<MODE>(A, raw, q);
-            const bool ok = products(q, raw.b, Sn, tid + 1, active, finish_next, yn);
-            if (active && finish_next && !ok) ++bad;
-            if (finish_next) centre_extras(raw, Sn);
-        }
-        // software pipelining: raw inputs of row jn+1 are in flight during the finish
-        if (finish_next && !(jn + 1 == ny && clamp_hi))
-            load_raw<MODE>(A, (long long)map_row(A, jn + 1) * pitch + ic, raw);
-        if (halo_side >= 0 && finish_next) {
-            cp_async_wait_all();
-            halo_products((jn - j0) & 1, Sn);
-            if (jn + 1 < j1) halo_fetch(jn + 1, (jn + 1 - j0) & 1);
-        }
-        // One barrier per row: makes row j's products (written one iteration
-        // ago, halo included) visible, and orders this iteration's writes to
-        // slot_next after the last reads of that slot (two rows ago).
-        __syncthreads();
-
-        // ---- finish row j -------------------------------------------------
-        const double* S = RING(slot_cur);
-        if (active) {
-            const double cy = ((j == 0 && clamp_lo) || (j == ny - 1 && clamp_hi)) ? A.c1y : A.cpy;
-            const double h = yc.h, u = yc.u, v = yc.v, w = yc.w, b = yc.b;
-            const double hv = yc.hv, v2 = yc.v2;
-            const int cc = tid + 1;
-            const double hu = S[XHU * SW + cc], u2 = S[XU2 * SW + cc];
-            const double r = S[CR * SW + cc], rh = S[CRH * SW + cc];
-#define DXQ(slot) sbp_d<POW2>(cx, S[(slot) * SW + sl], S[(slot) * SW + sr])
-#define DYQ(fld) sbp_d<POW2>(cy, yp.fld, yn.fld)
-            const double dh_x = DXQ(XH), du_x = DXQ(XU), dv_x = DXQ(XV);
-            const double dh_y = DYQ(h), du_y = DYQ(u), dv_y = DYQ(v);
-            const double de_x = DXQ(XE), de_y = DYQ(e);
-            const double db_x = DXQ(XB), db_y = DYQ(b);
-            const double g = A.g;
-            double o[5];
-            {  // continuity (rhs.hpp:156-157) + wall SAT (sbp.hpp:272-284)
-                const double s =
-                    dadd(dadd(dadd(dmul(u, dh_x), dmul(h, du_x)), dmul(v, dh_y)), dmul(h, dv_y));
-                double ht = -s;
-                if (A.walls) {
-                    double sat = 0.0;
-                    if (xl) sat = dsub(sat, dmul(A.tdx, hu));
-                    if (xr) sat = dadd(sat, dmul(A.tdx, hu));
-                    if (j == 0 && A.sat_y_lo) sat = dsub(sat, dmul(A.tdy, hv));
-                    if (j == ny - 1 && A.sat_y_hi) sat = dadd(sat, dmul(A.tdy, hv));
-                    ht = dadd(ht, sat);
-                }
-                o[0] = ht;
-            }
-            const double ghb = dmul(g, dadd(h, b));
-            const double ls_rr = dmul(A.lam_sixth, dmul(r, r));
-            const double lt_r = dmul(A.lam_third, r);
-            const double omr = dsub(1.0, r);
-            const double lh_omr = dmul(A.lam_half, omr);
-            const double uv = dmul(u, v);
-            {  // x-momentum (rhs.hpp:167-175), 0.5 factored out of the two split groups
-                const double du2_x = DXQ(XU2), dhu_x = DXQ(XHU), dhuv_y = DYQ(huv);
-                const double dhhb_x = DXQ(XHHB), de2h_x = DXQ(XE2H);
-                double s = dsub(dmul(g, dhhb_x), dmul(ghb, dh_x));
-                s = dadd(s, dmul(0.5, dsub(dadd(dsub(dmul(h, du2_x), dmul(u2, dh_x)), dmul(u, dhu_x)),
-                                           dmul(hu, du_x))));
-                s = dadd(s, dmul(0.5, dsub(dadd(dsub(dhuv_y, dmul(uv, dh_y)), dmul(hv, du_y)),
-                                           dmul(hu, dv_y))));
-                s = dadd(s, dadd(dsub(dsub(dadd(dmul(ls_rr, dh_x), dmul(A.lam_third, de_x)),
-                                           dmul(lt_r, de_x)),
-                                      dmul(A.lam_sixth, de2h_x)),
-                                 dmul(lh_omr, db_x)));
-                o[1] = div_by(-s, h, rh);
-            }
-            {  // y-momentum (rhs.hpp:180-188)
-                const double dv2_y = DYQ(v2), dhv_y = DYQ(hv), dhuv_x = DXQ(XHUV);
-                const double dhhb_y = DYQ(hhb), de2h_y = DYQ(e2h);
-                double s = dsub(dmul(g, dhhb_y), dmul(ghb, dh_y));
-                s = dadd(s, dmul(0.5, dsub(dadd(dsub(dmul(h, dv2_y), dmul(v2, dh_y)), dmul(v, dhv_y)),
-                                           dmul(hv, dv_y))));
-                s = dadd(s, dmul(0.5, dsub(dadd(dsub(dhuv_x, dmul(uv, dh_x)), dmul(hu, dv_x)),
-                                           dmul(hv, du_x))));
-                s = dadd(s, dadd(dsub(dsub(dadd(dmul(ls_rr, dh_y), dmul(A.lam_third, de_y)),
-                                           dmul(lt_r, de_y)),
-                                      dmul(A.lam_sixth, de2h_y)),
-                                 dmul(lh_omr, db_y)));
-                o[2] = div_by(-s, h, rh);
-            }
-            {  // vertical velocity (rhs.hpp:196-200)
-                const double dw_x = DXQ(XW), dhuw_x = DXQ(XHUW);
-                const double dw_y = DYQ(w), dhvw_y = DYQ(hvw);
-                const double hw = dmul(h, w);
-                double s = dmul(0.5, dsub(dsub(dadd(dhuw_x, dmul(hu, dw_x)), dmul(dmul(u, w), dh_x)),
-                                          dmul(hw, du_x)));
-                s = dadd(s, dmul(0.5, dsub(dsub(dadd(dhvw_y, dmul(hv, dw_y)), dmul(dmul(v, w), dh_y)),
-                                           dmul(hw, dv_y))));
-                o[3] = div_by(dsub(dmul(A.lambda, omr), s), h, rh);
-            }
-            {  // auxiliary depth (rhs.hpp:206-208)
-                const double s = dadd(dadd(dadd(dmul(u, de_x), dmul(v, de_y)), dmul(dmul(1.5, u), db_x)),
-                                      dmul(dmul(1.5, v), db_y));
-                o[4] = dsub(w, s);
-            }
-#undef DXQ
-#undef DYQ
-            if (A.shallow) {  // rhs_shallow_water zeroes the decoupled tendencies
-                o[3] = 0.0;
-                o[4] = 0.0;
-            }
-            if (A.source) {  // add_manufactured_sources: after assembly (rhs.hpp:212-213)
-                const double xg = dadd(A.x_min, dmul((double)i, A.dx));
-                const double yg = dadd(A.y_min, dmul((double)(A.j_global0 + j), A.dy));
-                double s5[5];
-                mms_source(A.t, xg, yg, A.g, s5);
-#pragma unroll
-                for (int f = 0; f < 5; ++f) o[f] = dadd(o[f], s5[f]);
-            }
-            // ---- epilogue
-            const long long off = (long long)j * pitch + i;
-            if (MODE == MODE_S2) {
-#pragma unroll
-                for (int f = 0; f < 5; ++f) {  // state_add3: ((y + c1 k1) + c2 k2) + c3 k3
-                    const double yn_f = dadd(S[(CYP0 + f) * SW + cc], dmul(A.c3, o[f]));
-                    A.out[f * A.fs + off] = yn_f;
-                    if (f == 0) {
-                        const unsigned long long bits = (unsigned long long)__double_as_longlong(yn_f);
-                        my_min = bits < my_min ? bits : my_min;
-                    }
-                }
-                if (A.adaptive) {  // ((d1 k1 + d2 k2) + d3 k3) for the error estimate
-#pragma unroll
-                    for (int f = 0; f < 5; ++f) {
-                        const double k1v = __ldg(A.kc + f * A.fs + off);
-                        const double k2v = __ldg(A.k + f * A.fs + off);
-                        A.part[f * A.fs + off] =
-                            dadd(dadd(dmul(A.d1, k1v), dmul(A.d2, k2v)), dmul(A.d3, o[f]));
-                    }
-                }
-            } else {
-#pragma unroll
-                for (int f = 0; f < 5; ++f) A.out[f * A.fs + off] = o[f];
-                if (MODE == MODE_S3 && A.adaptive) {
-                    // error_norm_and_min_h (time_integration.hpp:127-136)
-#pragma unroll
-                    for (int f = 0; f < 5; ++f) {
-                        const double e = dmul(A.dt, dadd(A.part[f * A.fs + off], dmul(A.d4, o[f])));
-                        const double ay = fabs(__ldg(A.yold + f * A.fs + off));
-                        const double an = fabs(__ldg(A.y + f * A.fs + off));
-                        const double scale = dadd(A.atol, dmul(A.rtol, ay < an ? an : ay));
-                        const double rq = e / scale;
-                        my_err = dadd(my_err, dmul(rq, rq));
-                    }
-                }
-            }
-        }
-        yp = yc;
-        yc = yn;
-        slot_cur = slot_next;
+    // ---- march, unrolled by 3: row j lives in ring slot (j-j0)%3 and register
+    // set {a,b,c}[(j-j0)%3]; step SC reads set SC+2 (row j-1), writes SC+1.
+    for (int j = j0; j < T.j1; j += 3) {
+        march_row<MODE, KIND, 0>(A, P, T, ring, j, yc, yb, raw);
+        if (j + 1 >= T.j1) break;
+        march_row<MODE, KIND, 1>(A, P, T, ring, j + 1, ya, yc, raw);
+        if (j + 2 >= T.j1) break;
+        march_row<MODE, KIND, 2>(A, P, T, ring, j + 2, yb, ya, raw);
     }
-    if (halo_side >= 0) cp_async_wait_all();
 
     // ---- block reductions (fixed order inside the block)
-    if (bad) atomicAdd(A.bad, bad);
+    if (T.bad) atomicAdd(A.bad, T.bad);
     const int warp = tid >> 5, lane = tid & 31;
     if (MODE == MODE_S2 && A.minh) {
-        const unsigned long long m = warp_min_u64(my_min);
+        const unsigned long long m = warp_min_u64(T.my_min);
         if (lane == 0) s_min[warp] = m;
         __syncthreads();
         if (tid == 0) {
@@ -477,7 +490,7 @@ __global__ void __launch_bounds__(BX, 3) sgn_stage_kernel(const StageArgs A) {
         }
     }
     if (MODE == MODE_S3 && A.adaptive) {
-        const double s = warp_sum(my_err);
+        const double s = warp_sum(T.my_err);
         if (lane == 0) s_err[warp] = s;
         __syncthreads();
         if (tid == 0) {
@@ -516,41 +529,52 @@ __global__ void __launch_bounds__(256) sum_partials_kernel(const double* part, i
 
 // ----------------------------------------------------------------- launch
 
-constexpr size_t RING_BYTES = sizeof(double) * 3 * NSMEM * SW;
+template <int MODE>
+__host__ __device__ constexpr size_t ring_bytes() { return sizeof(double2) * 3 * npairs<MODE>() * BX; }
 
-template <int MODE, bool POW2>
+template <int MODE, int KIND>
 static cudaError_t launch_mode(const StageArgs& A, cudaStream_t st) {
-    static bool configured = false;  // one-time opt-in above the 48 KB static limit
+    static bool configured = false;  // one-time opt-in above the 48 KB default
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(sgn_stage_kernel<MODE, POW2>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RING_BYTES);
+        cudaError_t e = cudaFuncSetAttribute(sgn_stage_kernel<MODE, KIND>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ring_bytes<MODE>());
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    dim3 grid((A.nx + BX - 1) / BX, (A.ny + A.rows_per_block - 1) / A.rows_per_block);
-    sgn_stage_kernel<MODE, POW2><<<grid, BX, RING_BYTES, st>>>(A);
+    KPtrs P;
+    for (int f = 0; f < 5; ++f) {
+        P.y[f] = A.y ? A.y + f * A.fs : nullptr;
+        P.k[f] = A.k ? A.k + f * A.fs : nullptr;
+        P.kc[f] = A.kc ? A.kc + f * A.fs : nullptr;
+        P.out[f] = A.out ? A.out + f * A.fs : nullptr;
+        P.part[f] = A.part ? A.part + f * A.fs : nullptr;
+        P.yold[f] = A.yold ? A.yold + f * A.fs : nullptr;
+    }
+    P.b = A.b;
+    dim3 grid((A.nx + WX - 1) / WX, (A.ny + A.rows_per_block - 1) / A.rows_per_block);
+    sgn_stage_kernel<MODE, KIND><<<grid, BX, ring_bytes<MODE>(), st>>>(A, P);
     return cudaGetLastError();
 }
 
-cudaError_t launch_stage(int mode, const StageArgs& A, cudaStream_t st) {
-    if (A.pow2) {
-        switch (mode) {
-            case MODE_RHS: return launch_mode<MODE_RHS, true>(A, st);
-            case MODE_S1: return launch_mode<MODE_S1, true>(A, st);
-            case MODE_S2: return launch_mode<MODE_S2, true>(A, st);
-            default: return launch_mode<MODE_S3, true>(A, st);
-        }
-    }
+template <int KIND>
+static cudaError_t launch_kind(int mode, const StageArgs& A, cudaStream_t st) {
     switch (mode) {
-        case MODE_RHS: return launch_mode<MODE_RHS, false>(A, st);
-        case MODE_S1: return launch_mode<MODE_S1, false>(A, st);
-        case MODE_S2: return launch_mode<MODE_S2, false>(A, st);
-        default: return launch_mode<MODE_S3, false>(A, st);
+        case MODE_RHS: return launch_mode<MODE_RHS, KIND>(A, st);
+        case MODE_S1: return launch_mode<MODE_S1, KIND>(A, st);
+        case MODE_S2: return launch_mode<MODE_S2, KIND>(A, st);
+        default: return launch_mode<MODE_S3, KIND>(A, st);
     }
 }
 
+// A.pow2 carries the stencil kind chosen by the host (see sbp_d).
+cudaError_t launch_stage(int mode, const StageArgs& A, cudaStream_t st) {
+    if (A.pow2 == 2) return launch_kind<2>(mode, A, st);
+    if (A.pow2 == 1) return launch_kind<1>(mode, A, st);
+    return launch_kind<0>(mode, A, st);
+}
+
 int stage_grid_blocks(const StageArgs& A) {
-    return ((A.nx + BX - 1) / BX) * ((A.ny + A.rows_per_block - 1) / A.rows_per_block);
+    return ((A.nx + WX - 1) / WX) * ((A.ny + A.rows_per_block - 1) / A.rows_per_block);
 }
 
 cudaError_t launch_sum_partials(const double* part, int n, double* out, cudaStream_t st) {

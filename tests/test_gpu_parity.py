@@ -179,3 +179,24 @@ def test_init_auxiliary_bitwise(orc):
         qs = H.StateField(g, q)
         H.init_auxiliary(ctx, qs)
         assert_equal_states(qs.flat(), want, "init_auxiliary")
+
+
+@pytest.mark.parametrize("kind", [0, 1, 2])
+def test_every_stencil_kind_bitwise(orc, kind):
+    """The three arithmetic variants (general / power-of-two / common factor)
+    must all reproduce the oracle on a grid where all three are valid."""
+    og = omake_grid(128, 128)
+    q, b = mms_exact_field(og, 0.3)
+    st, want, _ = orc.rhs(og, Phys(9.81, 500.0, 1e-12), b, q)
+    g = hgrid(og)
+    ctx = H.make_rhs_context(g, H.PhysSetup(9.81, 500.0, 1e-12, b.reshape(128, 128)))
+    assert ctx.stencil_kind == 2
+    ctx.stencil_kind = kind
+    assert ctx.stencil_kind == kind
+    out = H.StateField(g)
+    H.rhs(ctx, 0.0, H.StateField(g, q), out)
+    assert_equal_states(out.flat(), want, f"kind {kind}")
+    dt = 0.25 * g.dx / 20.0
+    want2, _ = orc.solve(og, Phys(9.81, 500.0, 1e-12), b, q, 0.0, 6 * dt, default_cfg(fixed_dt=dt))
+    res = H.adaptive_solve(ctx, H.StateField(g, q), 0.0, 6 * dt, H.IntegratorConfig(fixed_dt=dt))
+    assert_equal_states(res.q.flat(), want2, f"kind {kind} fixed steps")
