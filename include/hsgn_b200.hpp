@@ -1,0 +1,321 @@
+// hsgn_b200.hpp -- C++ drop-in mirror of the reference operator API
+// (/root/reference/proj/include/hsgn) for the time-stepping hot path, backed
+// by the sm_100a kernels through the C ABI in hsgn_b200.h.
+//
+// A caller of the reference switches by replacing
+//     #include <hsgn/rhs.hpp> / <hsgn/time_integration.hpp> / <hsgn/model.hpp>
+//     using namespace hsgn;
+// with
+//     #include <hsgn_b200.hpp>
+//     using namespace hsgn_b200;
+// and linking libhsgn_b200.so.  Names, argument meaning, storage layout
+// (StateField of row-major x-fastest fields) and error behaviour
+// (depth_error, std::invalid_argument, SolutionRecord abort reasons) follow
+// the reference; see INTEGRATION.md for the mapping table.  Two documented
+// differences:
+//   * the diagnostics take the context instead of explicit mass-weight
+//     vectors (the weights are derived from the context's grid exactly as
+//     build_d1 does, sbp.hpp:36-77);
+//   * adaptive_solve takes the context (its split-form RHS is fused into the
+//     stage kernels) instead of an arbitrary callable.
+#pragma once
+
+#include <array>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <functional>
+#include <limits>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "hsgn_b200.h"
+
+namespace hsgn_b200 {
+
+enum class BoundaryKind { periodic = HSGN_PERIODIC, bounded = HSGN_BOUNDED };  // grid.hpp:11
+
+struct depth_error : std::runtime_error {  // model.hpp:15-17
+    explicit depth_error(const std::string& w) : std::runtime_error(w) {}
+};
+
+struct device_error : std::runtime_error {
+    explicit device_error(const std::string& w) : std::runtime_error(w) {}
+};
+
+// Field2D (field.hpp:11-48): row-major, x fastest, index j*nx + i.
+class Field2D {
+public:
+    Field2D() = default;
+    Field2D(int nx, int ny, double fill = 0.0) : nx_(nx), ny_(ny), v_(static_cast<std::size_t>(nx) * ny, fill) {}
+    int nx() const { return nx_; }
+    int ny() const { return ny_; }
+    std::size_t size() const { return v_.size(); }
+    double& operator()(int i, int j) { return v_[static_cast<std::size_t>(j) * nx_ + i]; }
+    double operator()(int i, int j) const { return v_[static_cast<std::size_t>(j) * nx_ + i]; }
+    double& operator[](std::size_t k) { return v_[k]; }
+    double operator[](std::size_t k) const { return v_[k]; }
+    double* data() { return v_.data(); }
+    const double* data() const { return v_.data(); }
+    void fill(double value) { v_.assign(v_.size(), value); }
+    bool same_shape(const Field2D& o) const { return nx_ == o.nx_ && ny_ == o.ny_; }
+
+private:
+    int nx_ = 0, ny_ = 0;
+    std::vector<double> v_;
+};
+
+// Grid2D / make_grid (grid.hpp:16-68)
+struct Grid2D {
+    double x_min = 0.0, x_max = 1.0, y_min = 0.0, y_max = 1.0;
+    int nx = 0, ny = 0;
+    double dx = 0.0, dy = 0.0;
+    BoundaryKind kind_x = BoundaryKind::periodic, kind_y = BoundaryKind::periodic;
+    double x(int i) const { return x_min + i * dx; }
+    double y(int j) const { return y_min + j * dy; }
+    std::size_t n_total() const { return static_cast<std::size_t>(nx) * ny; }
+    Field2D make_field(double fill = 0.0) const { return Field2D(nx, ny, fill); }
+    template <class F>
+    Field2D sample(F&& f) const {
+        Field2D out(nx, ny);
+        for (int j = 0; j < ny; ++j)
+            for (int i = 0; i < nx; ++i) out(i, j) = f(x(i), y(j));
+        return out;
+    }
+    hsgn_grid c() const {
+        return hsgn_grid{nx, ny, static_cast<int32_t>(kind_x), static_cast<int32_t>(kind_y), x_min, x_max, y_min, y_max};
+    }
+};
+
+inline double direction_spacing(double lo, double hi, int n, BoundaryKind kind) {
+    return kind == BoundaryKind::periodic ? (hi - lo) / n : (hi - lo) / (n - 1);
+}
+
+inline Grid2D make_grid(double x_min, double x_max, double y_min, double y_max, int nx, int ny,
+                        BoundaryKind kind_x = BoundaryKind::periodic, BoundaryKind kind_y = BoundaryKind::periodic) {
+    if (!(x_max > x_min) || !(y_max > y_min))
+        throw std::invalid_argument("make_grid: domain extents must be increasing");
+    if (nx < 4 || ny < 4)
+        throw std::invalid_argument("make_grid: need at least 4 nodes per direction, got nx=" + std::to_string(nx) +
+                                    " ny=" + std::to_string(ny));
+    Grid2D g;
+    g.x_min = x_min;
+    g.x_max = x_max;
+    g.y_min = y_min;
+    g.y_max = y_max;
+    g.nx = nx;
+    g.ny = ny;
+    g.kind_x = kind_x;
+    g.kind_y = kind_y;
+    g.dx = direction_spacing(x_min, x_max, nx, kind_x);
+    g.dy = direction_spacing(y_min, y_max, ny, kind_y);
+    return g;
+}
+
+// StateField (model.hpp:22-35)
+struct StateField {
+    Field2D h, u, v, w, eta;
+    StateField() = default;
+    explicit StateField(const Grid2D& g)
+        : h(g.nx, g.ny), u(g.nx, g.ny), v(g.nx, g.ny), w(g.nx, g.ny), eta(g.nx, g.ny) {}
+    static constexpr int n_fields = 5;
+    std::array<Field2D*, n_fields> fields() { return {&h, &u, &v, &w, &eta}; }
+    std::array<const Field2D*, n_fields> fields() const { return {&h, &u, &v, &w, &eta}; }
+    static constexpr std::array<const char*, n_fields> names() { return {"h", "u", "v", "w", "eta"}; }
+};
+
+// PhysSetup (model.hpp:40-45)
+struct PhysSetup {
+    double g = 9.81;
+    double lambda = 500.0;
+    double h_floor = 1e-12;
+    Field2D b;
+};
+
+namespace detail {
+inline void pack(const StateField& s, std::vector<double>& buf) {
+    const std::size_t n = s.h.size();
+    buf.resize(5 * n);
+    auto f = s.fields();
+    for (int k = 0; k < 5; ++k) std::memcpy(buf.data() + k * n, f[k]->data(), n * sizeof(double));
+}
+inline void unpack(const std::vector<double>& buf, StateField& s) {
+    const std::size_t n = s.h.size();
+    auto f = s.fields();
+    for (int k = 0; k < 5; ++k) std::memcpy(f[k]->data(), buf.data() + k * n, n * sizeof(double));
+}
+}  // namespace detail
+
+// RhsContext (rhs.hpp:17-38) -> one device context.  Move-only, like the
+// reference context it must not be used by two host threads at once.
+class RhsContext {
+public:
+    Grid2D grid;
+    PhysSetup phys;
+
+    RhsContext(const Grid2D& g, const PhysSetup& p, int device = -1) : grid(g), phys(p) {
+        if (!phys.b.same_shape(Field2D(g.nx, g.ny)))
+            throw std::invalid_argument("make_rhs_context: bathymetry shape must match grid");
+        hsgn_grid cg = g.c();
+        hsgn_phys cp{p.g, p.lambda, p.h_floor};
+        const hsgn_status st = hsgn_ctx_create(&cg, &cp, phys.b.data(), device, &ctx_);
+        if (st == HSGN_EINVAL) throw std::invalid_argument("make_rhs_context: invalid grid or physics");
+        if (st != HSGN_OK) throw device_error("hsgn_ctx_create failed (is a B200 visible?)");
+    }
+    RhsContext(const RhsContext&) = delete;
+    RhsContext& operator=(const RhsContext&) = delete;
+    RhsContext(RhsContext&& o) noexcept : grid(o.grid), phys(std::move(o.phys)), ctx_(o.ctx_) { o.ctx_ = nullptr; }
+    ~RhsContext() {
+        for (hsgn_state* s : scratch_) hsgn_state_free(ctx_, s);
+        if (ctx_) hsgn_ctx_destroy(ctx_);
+    }
+
+    // ctx.source (rhs.hpp:24-26): the manufactured-solution forcing
+    void set_manufactured_source(bool on) { check(hsgn_set_source(ctx_, on ? 1 : 0), "set_source"); }
+    std::int64_t n_evals() const { return hsgn_n_evals(ctx_); }
+    hsgn_ctx* handle() const { return ctx_; }
+
+    void check(hsgn_status st, const char* what) const {
+        if (st == HSGN_OK) return;
+        const std::string msg = std::string(what) + ": " + hsgn_last_error(ctx_);
+        if (st == HSGN_EDEPTH) throw depth_error(msg);
+        if (st == HSGN_EINVAL) throw std::invalid_argument(msg);
+        throw device_error(msg);
+    }
+    hsgn_state* scratch(int k) {  // lazily allocated device states for host-facing calls
+        while (static_cast<int>(scratch_.size()) <= k) {
+            hsgn_state* s = nullptr;
+            check(hsgn_state_alloc(ctx_, &s), "state_alloc");
+            scratch_.push_back(s);
+        }
+        return scratch_[k];
+    }
+    void upload(const StateField& q, hsgn_state* s) {
+        detail::pack(q, buf_);
+        check(hsgn_state_upload(ctx_, s, buf_.data()), "upload");
+    }
+    void download(const hsgn_state* s, StateField& q) {
+        buf_.resize(5 * q.h.size());
+        check(hsgn_state_download(ctx_, s, buf_.data()), "download");
+        detail::unpack(buf_, q);
+    }
+
+private:
+    hsgn_ctx* ctx_ = nullptr;
+    std::vector<hsgn_state*> scratch_;
+    std::vector<double> buf_;
+};
+
+inline RhsContext make_rhs_context(const Grid2D& grid, const PhysSetup& phys) { return RhsContext(grid, phys); }
+
+// rhs / rhs_periodic / rhs_reflecting / rhs_shallow_water (rhs.hpp:219-248);
+// `t` only matters with the manufactured source.  Throws depth_error with out
+// untouched, as rhs.hpp:111-113.
+inline void rhs(RhsContext& ctx, double t, const StateField& q, StateField& out) {
+    ctx.upload(q, ctx.scratch(0));
+    int64_t bad = 0;
+    ctx.check(hsgn_rhs(ctx.handle(), t, ctx.scratch(0), ctx.scratch(1), &bad), "rhs");
+    ctx.download(ctx.scratch(1), out);
+}
+inline void rhs_periodic(RhsContext& ctx, double t, const StateField& q, StateField& out) { rhs(ctx, t, q, out); }
+inline void rhs_reflecting(RhsContext& ctx, double t, const StateField& q, StateField& out) { rhs(ctx, t, q, out); }
+inline void rhs_shallow_water(RhsContext& ctx, double t, const StateField& q, StateField& out) {
+    ctx.upload(q, ctx.scratch(0));
+    int64_t bad = 0;
+    ctx.check(hsgn_rhs_shallow_water(ctx.handle(), t, ctx.scratch(0), ctx.scratch(1), &bad), "rhs_shallow_water");
+    ctx.download(ctx.scratch(1), out);
+}
+
+// init_auxiliary (model.hpp:93-105), using the context's operators and b
+inline void init_auxiliary(RhsContext& ctx, StateField& q) {
+    ctx.upload(q, ctx.scratch(0));
+    ctx.check(hsgn_init_auxiliary(ctx.handle(), ctx.scratch(0)), "init_auxiliary");
+    ctx.download(ctx.scratch(0), q);
+}
+
+// total_mass / total_energy (model.hpp:77-87), energy_rate (analysis.hpp:47-67)
+inline double total_mass(RhsContext& ctx, const StateField& q) {
+    ctx.upload(q, ctx.scratch(0));
+    double m = 0.0;
+    ctx.check(hsgn_total_mass(ctx.handle(), ctx.scratch(0), &m), "total_mass");
+    return m;
+}
+inline double total_energy(RhsContext& ctx, const StateField& q) {
+    ctx.upload(q, ctx.scratch(0));
+    double e = 0.0;
+    ctx.check(hsgn_total_energy(ctx.handle(), ctx.scratch(0), &e), "total_energy");
+    return e;
+}
+inline double energy_rate(RhsContext& ctx, const StateField& q, const StateField& q_t) {
+    ctx.upload(q, ctx.scratch(0));
+    ctx.upload(q_t, ctx.scratch(1));
+    double r = 0.0;
+    ctx.check(hsgn_energy_rate(ctx.handle(), ctx.scratch(0), ctx.scratch(1), &r), "energy_rate");
+    return r;
+}
+
+// IntegratorConfig / SolutionRecord (time_integration.hpp:18-42)
+struct IntegratorConfig {
+    double abs_tol = 1e-6;
+    double rel_tol = 1e-6;
+    double dt_initial = 0.0;
+    double dt_max = std::numeric_limits<double>::infinity();
+    double safety = 0.9;
+    double growth_cap = 5.0;
+    double shrink_floor = 0.2;
+    std::int64_t max_steps = 50000000;
+    double fixed_dt = 0.0;
+    double h_floor = 1e-12;
+};
+
+struct SolutionRecord {
+    StateField q;
+    double t = 0.0;
+    std::int64_t accepted = 0, rejected = 0, rhs_evals = 0, rhs_evals_setup = 0;
+    bool aborted = false;
+    std::string abort_reason;
+};
+
+// AcceptObserver (time_integration.hpp:49); states are downloaded for the call.
+using AcceptObserver = std::function<void(double, const StateField&, const StateField&)>;
+
+namespace detail {
+struct ObsBox {
+    RhsContext* ctx;
+    const AcceptObserver* obs;
+    StateField q, qt;
+};
+inline void observer_tramp(double t, const hsgn_state* q, const hsgn_state* qt, void* user) {
+    ObsBox* b = static_cast<ObsBox*>(user);
+    b->ctx->download(q, b->q);
+    b->ctx->download(qt, b->qt);
+    (*b->obs)(t, b->q, b->qt);
+}
+}  // namespace detail
+
+// adaptive_solve (time_integration.hpp:209-350) on the fused stage kernels.
+inline SolutionRecord adaptive_solve(RhsContext& ctx, const StateField& q0, double t0, double t_final,
+                                     const IntegratorConfig& cfg, const AcceptObserver& on_accept = {}) {
+    hsgn_cfg c{cfg.abs_tol, cfg.rel_tol, cfg.dt_initial, cfg.dt_max,  cfg.safety,
+               cfg.growth_cap, cfg.shrink_floor, cfg.max_steps, cfg.fixed_dt, cfg.h_floor};
+    ctx.upload(q0, ctx.scratch(0));
+    hsgn_record r;
+    detail::ObsBox box{&ctx, &on_accept, StateField(ctx.grid), StateField(ctx.grid)};
+    ctx.check(hsgn_solve(ctx.handle(), ctx.scratch(0), t0, t_final, &c, ctx.scratch(1), &r,
+                         on_accept ? detail::observer_tramp : nullptr, &box),
+              "adaptive_solve");
+    SolutionRecord rec;
+    rec.q = StateField(ctx.grid);
+    ctx.download(ctx.scratch(1), rec.q);
+    rec.t = r.t;
+    rec.accepted = r.accepted;
+    rec.rejected = r.rejected;
+    rec.rhs_evals = r.rhs_evals;
+    rec.rhs_evals_setup = r.rhs_evals_setup;
+    rec.aborted = r.aborted != 0;
+    rec.abort_reason = r.reason;
+    return rec;
+}
+
+}  // namespace hsgn_b200

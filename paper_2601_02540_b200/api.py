@@ -351,6 +351,14 @@ def energy_rate(ctx: RhsContext, q, q_t) -> float:
     return _reduce(ctx, N.lib().hsgn_energy_rate, q, q_t)
 
 
+def mass_weighted_sum(ctx: RhsContext, q, field_index: int) -> float:
+    """sbp.hpp:219-239 of one field of a state (SBP-norm quadrature)."""
+    dq = _as_device(ctx, q)[0]
+    out = C.c_double(0.0)
+    _check(ctx, N.lib().hsgn_mass_weighted_sum(ctx._h, dq._h, field_index, C.byref(out)), "mass_weighted_sum")
+    return out.value
+
+
 def discrete_l2_error(ctx: RhsContext, a, b, field_index: int) -> float:
     da, db = _as_device(ctx, a)[0], _as_device(ctx, b)[0]
     out = C.c_double(0.0)

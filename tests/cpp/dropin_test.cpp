@@ -1,0 +1,162 @@
+// dropin_test.cpp -- the reference's own RHS / integrator test cases
+// (proj/tests/test_rhs.cpp, test_time_integration.cpp), rewritten against the
+// C++ drop-in header: only the include and the namespace differ from a
+// reference caller.  Built and run by tests/test_cpp_dropin.py on a B200.
+#include <hsgn_b200.hpp>
+
+#include <cmath>
+#include <cstdio>
+#include <random>
+
+using namespace hsgn_b200;
+
+static int failures = 0;
+#define CHECK(cond)                                                   \
+    do {                                                              \
+        if (!(cond)) {                                                \
+            std::printf("FAIL %s:%d: %s\n", __FILE__, __LINE__, #cond); \
+            ++failures;                                               \
+        }                                                             \
+    } while (0)
+
+static RhsContext context_on(const Grid2D& g, double lambda, const std::function<double(double, double)>& bathy) {
+    PhysSetup phys;
+    phys.lambda = lambda;
+    phys.b = g.sample(bathy);
+    return RhsContext(g, phys);
+}
+
+static void randomize(StateField& q, unsigned seed) {  // test_rhs.cpp:22-33
+    std::mt19937 rng(seed);
+    std::uniform_real_distribution<double> depth(0.5, 1.5), vel(-1.0, 1.0);
+    for (std::size_t k = 0; k < q.h.size(); ++k) {
+        q.h[k] = depth(rng);
+        q.u[k] = vel(rng);
+        q.v[k] = vel(rng);
+        q.w[k] = vel(rng);
+        q.eta[k] = depth(rng);
+    }
+}
+
+static double mass_sum(const Grid2D& g, const Field2D& f) {  // sbp.hpp:219-239 weights, plain sum
+    double s = 0.0;
+    for (int j = 0; j < g.ny; ++j)
+        for (int i = 0; i < g.nx; ++i) {
+            double wx = g.dx, wy = g.dy;
+            if (g.kind_x == BoundaryKind::bounded && (i == 0 || i == g.nx - 1)) wx *= 0.5;
+            if (g.kind_y == BoundaryKind::bounded && (j == 0 || j == g.ny - 1)) wy *= 0.5;
+            s += wx * wy * f(i, j);
+        }
+    return s;
+}
+
+int main() {
+    auto flat = [](double, double) { return 0.0; };
+    {  // uniform columns are steady (test_rhs.cpp:39-65)
+        Grid2D g = make_grid(-1.0, 1.0, -1.0, 1.0, 12, 10);
+        RhsContext ctx = context_on(g, 500.0, flat);
+        StateField q(g), out(g);
+        q.h.fill(1.0);
+        q.u.fill(0.3);
+        q.v.fill(-0.7);
+        q.eta.fill(1.0);
+        rhs_periodic(ctx, 0.0, q, out);
+        for (Field2D* f : out.fields())
+            for (std::size_t k = 0; k < f->size(); ++k) CHECK((*f)[k] == 0.0);
+        Grid2D gb = make_grid(-1.0, 1.0, -1.0, 1.0, 12, 10, BoundaryKind::bounded, BoundaryKind::bounded);
+        RhsContext cb = context_on(gb, 500.0, flat);
+        StateField qb(gb), ob(gb);
+        qb.h.fill(2.0);
+        qb.eta.fill(2.0);
+        rhs_reflecting(cb, 0.0, qb, ob);
+        for (Field2D* f : ob.fields())
+            for (std::size_t k = 0; k < f->size(); ++k) CHECK((*f)[k] == 0.0);
+    }
+    {  // lake at rest over a bump (test_rhs.cpp:67-82)
+        auto bump = [](double x, double y) { return 0.1 * std::exp(-(x * x + y * y)); };
+        for (BoundaryKind kind : {BoundaryKind::periodic, BoundaryKind::bounded}) {
+            Grid2D g = make_grid(-5.0, 5.0, -5.0, 5.0, 33, 33, kind, kind);
+            RhsContext ctx = context_on(g, 500.0, bump);
+            StateField q(g), out(g);
+            for (std::size_t k = 0; k < q.h.size(); ++k) q.h[k] = 1.0 - ctx.phys.b[k];
+            init_auxiliary(ctx, q);
+            rhs(ctx, 0.0, q, out);
+            for (Field2D* f : out.fields())
+                for (std::size_t k = 0; k < f->size(); ++k) CHECK(std::abs((*f)[k]) <= 1e-12 * 9.81);
+        }
+    }
+    {  // mass invariance (test_rhs.cpp:84-106) and energy rate (108-127)
+        Grid2D g = make_grid(-1.0, 1.0, -1.0, 1.0, 24, 20, BoundaryKind::bounded, BoundaryKind::bounded);
+        RhsContext ctx = context_on(g, 500.0, [](double x, double y) { return 0.05 * std::cos(x - y); });
+        StateField q(g), out(g);
+        randomize(q, 12);
+        rhs_reflecting(ctx, 0.0, q, out);
+        CHECK(std::abs(mass_sum(g, out.h)) <= 1e-12);
+        const double e = total_energy(ctx, q);
+        CHECK(std::abs(energy_rate(ctx, q, out)) <= 1e-11 * std::abs(e));
+    }
+    {  // determinism (test_rhs.cpp:159-174)
+        Grid2D g = make_grid(-1.0, 1.0, -1.0, 1.0, 20, 20, BoundaryKind::bounded, BoundaryKind::periodic);
+        RhsContext ctx = context_on(g, 500.0, [](double x, double y) { return 0.03 * std::sin(x * y); });
+        StateField q(g), a(g), b(g);
+        randomize(q, 41);
+        rhs(ctx, 0.5, q, a);
+        rhs(ctx, 0.5, q, b);
+        auto fa = a.fields();
+        auto fb = b.fields();
+        for (int f = 0; f < 5; ++f)
+            for (std::size_t k = 0; k < fa[f]->size(); ++k) CHECK((*fa[f])[k] == (*fb[f])[k]);
+        CHECK(ctx.n_evals() == 2);
+    }
+    {  // non-positive depth raises (test_rhs.cpp:176-186)
+        Grid2D g = make_grid(-1.0, 1.0, -1.0, 1.0, 8, 8);
+        RhsContext ctx = context_on(g, 500.0, flat);
+        StateField q(g), out(g);
+        q.h.fill(1.0);
+        q.eta.fill(1.0);
+        q.h(3, 4) = -0.25;
+        bool threw = false;
+        try {
+            rhs(ctx, 0.0, q, out);
+        } catch (const depth_error&) {
+            threw = true;
+        }
+        CHECK(threw);
+    }
+    {  // invalid grids throw like grid.hpp:51-55
+        bool threw = false;
+        try {
+            make_grid(0.0, 1.0, 0.0, 1.0, 3, 8);
+        } catch (const std::invalid_argument&) {
+            threw = true;
+        }
+        CHECK(threw);
+    }
+    {  // integrator: ledger, observer, mass through full steps (test_time_integration.cpp:127-150, 290-307)
+        Grid2D g = make_grid(-5.0, 5.0, -5.0, 5.0, 32, 32);
+        RhsContext ctx = context_on(g, 500.0, flat);
+        StateField q0(g);
+        q0.h = g.sample([](double x, double y) { return 1.0 + 0.1 * std::exp(-(x * x + y * y)); });
+        init_auxiliary(ctx, q0);
+        const double m0 = total_mass(ctx, q0);
+        std::vector<double> times;
+        IntegratorConfig cfg;
+        SolutionRecord rec =
+            adaptive_solve(ctx, q0, 0.0, 0.1, cfg, [&](double t, const StateField&, const StateField&) { times.push_back(t); });
+        CHECK(!rec.aborted);
+        CHECK(rec.t == 0.1);
+        CHECK(times.size() == static_cast<std::size_t>(rec.accepted) + 1);
+        CHECK(rec.rhs_evals == 3 * (rec.accepted + rec.rejected) + 1 + rec.rhs_evals_setup);
+        CHECK(std::abs(total_mass(ctx, rec.q) - m0) <= 1e-12 * std::abs(m0));
+        SolutionRecord back = adaptive_solve(ctx, q0, 2.0, 1.0, cfg);
+        CHECK(back.aborted && back.abort_reason.find("precedes") != std::string::npos);
+        IntegratorConfig one;
+        one.max_steps = 1;
+        one.dt_initial = 1e-3;
+        SolutionRecord budget = adaptive_solve(ctx, q0, 0.0, 100.0, one);
+        CHECK(budget.aborted && budget.abort_reason.find("step budget exhausted") != std::string::npos);
+        CHECK(budget.accepted == 1);
+    }
+    std::printf("%s (%d failures)\n", failures ? "FAILED" : "PASSED", failures);
+    return failures ? 1 : 0;
+}
