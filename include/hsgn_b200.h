@@ -117,6 +117,13 @@ hsgn_status hsgn_set_rows_per_block(hsgn_ctx* ctx, int32_t rows);
 hsgn_status hsgn_set_stencil_kind(hsgn_ctx* ctx, int32_t kind);
 int32_t hsgn_stencil_kind(const hsgn_ctx* ctx);
 
+/* Raw-input staging: 1 = TMA bulk copies into a shared-memory ring two rows
+ * ahead (needs nx even), 0 = register prefetch one row ahead (default: it
+ * measured faster in round 1).  Both are bit-identical;
+ * the switch exists for tests and measurements. */
+hsgn_status hsgn_set_tma(hsgn_ctx* ctx, int32_t on);
+int32_t hsgn_tma_enabled(const hsgn_ctx* ctx);
+
 /* ctx.n_evals (rhs.hpp:28,84) */
 int64_t hsgn_n_evals(const hsgn_ctx* ctx);
 

@@ -75,6 +75,8 @@ def lib() -> C.CDLL:
     f("hsgn_set_rows_per_block", C.c_int, CTX, I32)
     f("hsgn_set_stencil_kind", C.c_int, CTX, I32)
     f("hsgn_stencil_kind", I32, CTX)
+    f("hsgn_set_tma", C.c_int, CTX, I32)
+    f("hsgn_tma_enabled", I32, CTX)
     f("hsgn_n_evals", I64, CTX)
     f("hsgn_state_alloc", C.c_int, CTX, PST)
     f("hsgn_state_free", C.c_int, CTX, STATE)
@@ -106,7 +108,7 @@ def lib() -> C.CDLL:
 EXPORTS = [
     "hsgn_ctx_create", "hsgn_ctx_create_slab", "hsgn_nccl_unique_id", "hsgn_ctx_attach_nccl",
     "hsgn_ctx_destroy", "hsgn_last_error", "hsgn_set_source", "hsgn_set_rows_per_block",
-    "hsgn_set_stencil_kind", "hsgn_stencil_kind", "hsgn_n_evals",
+    "hsgn_set_stencil_kind", "hsgn_stencil_kind", "hsgn_set_tma", "hsgn_tma_enabled", "hsgn_n_evals",
     "hsgn_state_alloc", "hsgn_state_free", "hsgn_state_upload", "hsgn_state_download", "hsgn_state_copy",
     "hsgn_state_field_ptr", "hsgn_rhs", "hsgn_rhs_shallow_water", "hsgn_init_auxiliary", "hsgn_solve",
     "hsgn_bs3_fixed_steps", "hsgn_total_mass", "hsgn_total_energy", "hsgn_energy_rate",

@@ -263,6 +263,15 @@ class RhsContext:
     def stencil_kind(self, kind: int):
         _check(self, N.lib().hsgn_set_stencil_kind(self._h, int(kind)), "hsgn_set_stencil_kind")
 
+    @property
+    def tma(self) -> bool:
+        """Raw inputs staged by TMA bulk copies (True) or register prefetch."""
+        return bool(N.lib().hsgn_tma_enabled(self._h))
+
+    @tma.setter
+    def tma(self, on: bool):
+        _check(self, N.lib().hsgn_set_tma(self._h, int(bool(on))), "hsgn_set_tma")
+
     def state(self, host=None) -> DeviceState:
         return DeviceState(self, host)
 

@@ -126,6 +126,7 @@ struct hsgn_ctx {
     int source = 0;
     int rows_per_block = 0;
     int forced_kind = -1;  // stencil kind override (tests); -1 = automatic
+    int use_tma = 0;       // TMA staging of raw inputs when nx is even (opt-in: slower in r1)
     int64_t n_evals = 0;
     std::string err;
     // workspace for the integrator
@@ -236,6 +237,7 @@ static hsgn_status setup_ctx(hsgn_ctx* c) {
     const bool cf = p2 && A.cpx == A.cpy && !A.x_bounded && A.y_lo != YE_CLAMP && A.y_hi != YE_CLAMP && !A.walls;
     A.pow2 = cf ? 2 : (p2 ? 1 : 0);
     if (c->forced_kind >= 0 && c->forced_kind < A.pow2) A.pow2 = c->forced_kind;
+    A.tma = c->use_tma && (g.nx % 2 == 0);
     A.g = c->phys.g;
     A.lambda = c->phys.lambda;
     A.lam_half = c->phys.lambda / 2.0;
@@ -668,6 +670,14 @@ hsgn_status hsgn_set_stencil_kind(hsgn_ctx* c, int32_t kind) {
 }
 
 int32_t hsgn_stencil_kind(const hsgn_ctx* c) { return c ? c->base.pow2 : -1; }
+
+hsgn_status hsgn_set_tma(hsgn_ctx* c, int32_t on) {
+    if (!c) return HSGN_EINVAL;
+    c->use_tma = on ? 1 : 0;
+    return reconfigure(c);
+}
+
+int32_t hsgn_tma_enabled(const hsgn_ctx* c) { return c ? c->base.tma : 0; }
 
 int64_t hsgn_n_evals(const hsgn_ctx* c) { return c ? c->n_evals : 0; }
 

@@ -225,6 +225,93 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
+// ------------------------------------------------------------ TMA staging
+// Bulk-async (TMA) prefetch of the raw stage inputs into a 3-slot shared
+// ring, two rows ahead of use.  One elected thread issues, per row and input
+// field, 1-3 cp.async.bulk copies (the tile's columns i0-2 .. i0+127 with the
+// periodic wrap split off) completing on the slot's mbarrier; all threads
+// wait on the mbarrier phase before reading their column.  Requires nx even
+// (16-byte aligned pieces); the host falls back to register prefetch
+// otherwise.
+constexpr int RW = BX + 2;  // raw row width: logical columns i0-2 .. i0+127
+constexpr int RSLOTS = 3;
+
+template <int MODE>
+__host__ __device__ constexpr int nraw() { return MODE == MODE_S2 ? 16 : (MODE == MODE_S1 ? 11 : 6); }
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_copy(double* dst, const double* src, unsigned bytes, unsigned long long* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+// Issue the raw inputs of logical row jr for the tile starting at column i0
+// into ring slot `slot` (layout [field][RW]).  Called by one thread.
+template <int MODE>
+__device__ __forceinline__ void tma_issue_row(const StageArgs& A, const KPtrs& P, int jr, int i0, double* slot,
+                                              unsigned long long* bar) {
+    const int nx = A.nx;
+    const long long row = (long long)map_row(A, jr) * nx;
+    int lo = i0 - 2, hi = i0 + BX;  // logical columns [lo, hi)
+    // pieces (smem offset, global column, length), all even
+    int po[3], pg[3], pl[3], np = 0;
+    if (A.x_bounded) {
+        const int a = lo < 0 ? 0 : lo, b = hi > nx ? nx : hi;
+        po[np] = a - lo; pg[np] = a; pl[np] = b - a; ++np;
+    } else {
+        if (hi > nx + 2) hi = nx + 2;  // beyond column nx only idle lanes
+        if (lo < 0) { po[np] = 0; pg[np] = nx + lo; pl[np] = -lo; ++np; }
+        const int a = lo < 0 ? 0 : lo, b = hi > nx ? nx : hi;
+        po[np] = a - lo; pg[np] = a; pl[np] = b - a; ++np;
+        if (hi > nx) { po[np] = nx - lo; pg[np] = 0; pl[np] = hi - nx; ++np; }
+    }
+    int cols = 0;
+    for (int k = 0; k < np; ++k) cols += pl[k];
+    mbar_expect_tx(bar, (unsigned)(cols * 8 * nraw<MODE>()));
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads of the slot
+#pragma unroll
+    for (int f = 0; f < nraw<MODE>(); ++f) {
+        const double* base = f < 5 ? P.y[f] : (f == nraw<MODE>() - 1 ? P.b : (f < 10 ? P.k[f - 5] : P.kc[f - 10]));
+        for (int k = 0; k < np; ++k)
+            tma_copy(slot + f * RW + po[k], base + row + pg[k], (unsigned)(pl[k] * 8), bar);
+    }
+}
+
+// Read this thread's column of a raw slot into the Raw struct.
+template <int MODE>
+__device__ __forceinline__ void raw_from_smem(const double* slot, int tid, Raw& r) {
+    const double* s = slot + tid + 1;
+#pragma unroll
+    for (int f = 0; f < 5; ++f) r.y[f] = s[f * RW];
+    if (MODE == MODE_S1 || MODE == MODE_S2) {
+#pragma unroll
+        for (int f = 0; f < 5; ++f) r.k[f] = s[(5 + f) * RW];
+    }
+    if (MODE == MODE_S2) {
+#pragma unroll
+        for (int f = 0; f < 5; ++f) r.kc[f] = s[(10 + f) * RW];
+    }
+    r.b = s[(nraw<MODE>() - 1) * RW];
+}
+
 // Per-thread constants and accumulators of one CTA's march.
 struct Thr {
     int tid, i, j1;
@@ -260,19 +347,33 @@ __device__ __forceinline__ void neighbour_x(const double2* S, XQ& X) {
 
 // One row of the march: form row jn = j+1 (ring slot SN, register set yn),
 // then finish row j (ring slot SC; row j-1 is register set yp).
-template <int MODE, int KIND, int SC>
-__device__ __forceinline__ void march_row(const StageArgs& A, const KPtrs& P, Thr& T, double2* ring, int j,
-                                          const YQ& yp, YQ& yn, Raw& raw) {
+template <int MODE, int KIND, bool TMA, int SC>
+__device__ __forceinline__ void march_row(const StageArgs& A, const KPtrs& P, Thr& T, double2* ring, double* rawring,
+                                          unsigned long long* bars, int j0, int j, const YQ& yp, YQ& yn, Raw& raw,
+                                          Raw& raw_next) {
     constexpr int NP = npairs<MODE>();
     constexpr int SN = (SC + 1) % 3;
     const int jn = j + 1;
     const unsigned nx = (unsigned)A.nx;
+    // register prefetch of raw(jn+1), issued after products(jn) so the load is
+    // in flight during the finish of row j.  (Issuing it before products(jn)
+    // needs two raw register sets and a 6x-unrolled march: measured slower in
+    // round 1 -- spills in S1/S2, I-cache in S3 -- so EARLY stays off; raw and
+    // raw_next may then alias.)
+    constexpr bool EARLY = false;
+    if (!TMA && EARLY && jn < T.j1) load_raw<MODE>(P, (unsigned)map_row(A, jn + 1) * nx + T.col, raw_next);
+    if (TMA) {  // raw row jn lives in raw slot (SC+2)%3; row j+3 goes into slot (SC+1)%3
+        constexpr int RS = (SC + 2) % 3, RI = (SC + 1) % 3;
+        mbar_wait(&bars[RS], (unsigned)(((jn - j0 + 1) / 3) & 1));
+        raw_from_smem<MODE>(rawring + RS * (nraw<MODE>() * RW), T.tid, raw);
+        if (T.tid == 0 && j + 3 <= T.j1)
+            tma_issue_row<MODE>(A, P, j + 3, (int)blockIdx.x * WX, rawring + RI * (nraw<MODE>() * RW), &bars[RI]);
+    }
     {  // products of row jn (for D_y of row j, and D_x of row jn one step later)
         const bool ok = products<MODE>(A, raw, ring + SN * (NP * BX) + T.tid, yn);
         if (T.finish && jn < T.j1 && !ok) ++T.bad;
     }
-    // software pipelining: raw inputs of row jn+1 are in flight during the finish
-    if (jn < T.j1) load_raw<MODE>(P, (unsigned)map_row(A, jn + 1) * nx + T.col, raw);
+    if (!TMA && !EARLY && jn < T.j1) load_raw<MODE>(P, (unsigned)map_row(A, jn + 1) * nx + T.col, raw_next);
     // One barrier per row: row j's ring entries (written one step ago) become
     // visible, and this step's writes to slot SN are ordered after the last
     // reads of that slot (finish of row j-2, before the previous barrier).
@@ -403,7 +504,7 @@ __device__ __forceinline__ void march_row(const StageArgs& A, const KPtrs& P, Th
     }
 }
 
-template <int MODE, int KIND>
+template <int MODE, int KIND, bool TMA>
 __global__ void __launch_bounds__(BX, min_blocks<MODE>()) sgn_stage_kernel(const StageArgs A, const KPtrs P) {
     constexpr int NP = npairs<MODE>();
     extern __shared__ __align__(16) double2 ring[];  // 3 x NP x BX pairs
@@ -457,23 +558,50 @@ __global__ void __launch_bounds__(BX, min_blocks<MODE>()) sgn_stage_kernel(const
     // ---- prologue: row j0-1 -> register set C (ring slot 2), row j0 -> set A (slot 0)
     YQ ya, yb, yc;
     Raw raw;
-    load_raw<MODE>(P, (unsigned)map_row(A, j0 - 1) * unx + T.col, raw);
+    double* rawring = reinterpret_cast<double*>(ring + 3 * NP * BX);  // TMA: RSLOTS x nraw x RW
+    __shared__ __align__(8) unsigned long long bars[RSLOTS];
+    if (TMA) {  // raw row r lives in slot (r - j0 + 1) % 3
+        const int i0 = (int)blockIdx.x * WX;
+        if (tid == 0) {
+            for (int s = 0; s < RSLOTS; ++s) mbar_init(&bars[s], 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            for (int s = 0; s < RSLOTS; ++s)
+                if (j0 - 1 + s <= T.j1)
+                    tma_issue_row<MODE>(A, P, j0 - 1 + s, i0, rawring + s * (nraw<MODE>() * RW), &bars[s]);
+        }
+        __syncthreads();
+        mbar_wait(&bars[0], 0);
+        raw_from_smem<MODE>(rawring, tid, raw);
+    } else {
+        load_raw<MODE>(P, (unsigned)map_row(A, j0 - 1) * unx + T.col, raw);
+    }
     products<MODE>(A, raw, ring + 2 * (NP * BX) + tid, yc);
-    load_raw<MODE>(P, (unsigned)j0 * unx + T.col, raw);
+    if (TMA) {
+        mbar_wait(&bars[1], 0);
+        raw_from_smem<MODE>(rawring + nraw<MODE>() * RW, tid, raw);
+    } else {
+        load_raw<MODE>(P, (unsigned)j0 * unx + T.col, raw);
+    }
     {
         const bool ok = products<MODE>(A, raw, ring + tid, ya);
         if (T.finish && !ok) ++T.bad;
     }
-    load_raw<MODE>(P, (unsigned)map_row(A, j0 + 1) * unx + T.col, raw);
+    if (TMA) {  // slot 0 (row j0-1) is free once every thread has read it
+        __syncthreads();
+        if (tid == 0 && j0 + 2 <= T.j1)
+            tma_issue_row<MODE>(A, P, j0 + 2, (int)blockIdx.x * WX, rawring, &bars[0]);
+    } else {
+        load_raw<MODE>(P, (unsigned)map_row(A, j0 + 1) * unx + T.col, raw);
+    }
 
     // ---- march, unrolled by 3: row j lives in ring slot (j-j0)%3 and register
     // set {a,b,c}[(j-j0)%3]; step SC reads set SC+2 (row j-1), writes SC+1.
     for (int j = j0; j < T.j1; j += 3) {
-        march_row<MODE, KIND, 0>(A, P, T, ring, j, yc, yb, raw);
+        march_row<MODE, KIND, TMA, 0>(A, P, T, ring, rawring, bars, j0, j, yc, yb, raw, raw);
         if (j + 1 >= T.j1) break;
-        march_row<MODE, KIND, 1>(A, P, T, ring, j + 1, ya, yc, raw);
+        march_row<MODE, KIND, TMA, 1>(A, P, T, ring, rawring, bars, j0, j + 1, ya, yc, raw, raw);
         if (j + 2 >= T.j1) break;
-        march_row<MODE, KIND, 2>(A, P, T, ring, j + 2, yb, ya, raw);
+        march_row<MODE, KIND, TMA, 2>(A, P, T, ring, rawring, bars, j0, j + 2, yb, ya, raw, raw);
     }
 
     // ---- block reductions (fixed order inside the block)
@@ -529,18 +657,28 @@ __global__ void __launch_bounds__(256) sum_partials_kernel(const double* part, i
 
 // ----------------------------------------------------------------- launch
 
-template <int MODE>
-__host__ __device__ constexpr size_t ring_bytes() { return sizeof(double2) * 3 * npairs<MODE>() * BX; }
+template <int MODE, bool TMA>
+__host__ __device__ constexpr size_t ring_bytes() {
+    return sizeof(double2) * 3 * npairs<MODE>() * BX + (TMA ? sizeof(double) * RSLOTS * nraw<MODE>() * RW : 0);
+}
 
-template <int MODE, int KIND>
-static cudaError_t launch_mode(const StageArgs& A, cudaStream_t st) {
+template <int MODE, int KIND, bool TMA>
+static cudaError_t launch_tma(const StageArgs& A, const KPtrs& P, cudaStream_t st) {
     static bool configured = false;  // one-time opt-in above the 48 KB default
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(sgn_stage_kernel<MODE, KIND>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ring_bytes<MODE>());
+        cudaError_t e = cudaFuncSetAttribute(sgn_stage_kernel<MODE, KIND, TMA>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)ring_bytes<MODE, TMA>());
         if (e != cudaSuccess) return e;
         configured = true;
     }
+    dim3 grid((A.nx + WX - 1) / WX, (A.ny + A.rows_per_block - 1) / A.rows_per_block);
+    sgn_stage_kernel<MODE, KIND, TMA><<<grid, BX, ring_bytes<MODE, TMA>(), st>>>(A, P);
+    return cudaGetLastError();
+}
+
+template <int MODE, int KIND>
+static cudaError_t launch_mode(const StageArgs& A, cudaStream_t st) {
     KPtrs P;
     for (int f = 0; f < 5; ++f) {
         P.y[f] = A.y ? A.y + f * A.fs : nullptr;
@@ -551,9 +689,9 @@ static cudaError_t launch_mode(const StageArgs& A, cudaStream_t st) {
         P.yold[f] = A.yold ? A.yold + f * A.fs : nullptr;
     }
     P.b = A.b;
-    dim3 grid((A.nx + WX - 1) / WX, (A.ny + A.rows_per_block - 1) / A.rows_per_block);
-    sgn_stage_kernel<MODE, KIND><<<grid, BX, ring_bytes<MODE>(), st>>>(A, P);
-    return cudaGetLastError();
+    // TMA staging needs 16-byte aligned row pieces: nx even (host decides)
+    if (A.tma && (A.nx % 2) == 0) return launch_tma<MODE, KIND, true>(A, P, st);
+    return launch_tma<MODE, KIND, false>(A, P, st);
 }
 
 template <int KIND>

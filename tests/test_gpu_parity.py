@@ -181,6 +181,32 @@ def test_init_auxiliary_bitwise(orc):
         assert_equal_states(qs.flat(), want, "init_auxiliary")
 
 
+@pytest.mark.parametrize("nx,ny,kx,ky", [(64, 40, 0, 0), (130, 33, 0, 0), (256, 70, 0, 1), (254, 20, 1, 0),
+                                         (1000, 12, 1, 1), (126, 9, 0, 0), (252, 17, 0, 0)])
+@pytest.mark.parametrize("tma", [True, False])
+def test_raw_staging_variants_bitwise(orc, nx, ny, kx, ky, tma):
+    """TMA bulk staging (periodic wrap pieces, bounded clipping, partial last
+    tiles) and register prefetch give the oracle's bits, RHS and 5 steps."""
+    og = omake_grid(nx, ny, kind_x=kx, kind_y=ky)
+    q, b = mms_exact_field(og, 0.3)
+    ph = Phys(9.81, 500.0, 1e-12)
+    st, want, _ = orc.rhs(og, ph, b, q)
+    g = hgrid(og)
+    ctx = H.make_rhs_context(g, H.PhysSetup(9.81, 500.0, 1e-12, b.reshape(ny, nx)))
+    ctx.tma = tma
+    assert ctx.tma == tma
+    out = H.StateField(g)
+    H.rhs(ctx, 0.0, H.StateField(g, q), out)
+    assert_equal_states(out.flat(), want, f"rhs tma={tma}")
+    dx = 2.0 / (nx - 1 if kx else nx)
+    dt = 0.25 * dx / 20.0
+    T = 5 * dt
+    want2, rec = orc.solve(og, ph, b, q, 0.0, T, default_cfg(fixed_dt=dt))
+    res = H.adaptive_solve(ctx, H.StateField(g, q), 0.0, T, H.IntegratorConfig(fixed_dt=dt))
+    assert res.accepted == rec.accepted
+    assert_equal_states(res.q.flat(), want2, f"steps tma={tma}")
+
+
 @pytest.mark.parametrize("kind", [0, 1, 2])
 def test_every_stencil_kind_bitwise(orc, kind):
     """The three arithmetic variants (general / power-of-two / common factor)
