@@ -322,7 +322,26 @@ struct Thr {
     int jc0, jc1;       // rows that use the y closure coefficient (clamped walls)
     unsigned long long bad, my_min;
     double my_err;
+    // L2 prefetch (thread f < nraw owns raw field f): field base, tile span
+    const double* pf_base;
+    int pf_col, pf_bytes;
 };
+
+// Distance (rows) of the bulk L2 prefetch ahead of the register loads.
+#ifndef HSGN_L2_PF
+#define HSGN_L2_PF 0
+#endif
+
+// One cp.async.bulk.prefetch.L2 per raw field and row: the tile's row segment
+// is pulled into L2 HSGN_L2_PF rows before the register loads touch it, so
+// those loads see L2 instead of DRAM latency.  No registers or shared memory.
+template <int MODE>
+__device__ __forceinline__ void l2_prefetch_row(const StageArgs& A, const Thr& T, int jr) {
+    if (T.pf_bytes > 0) {
+        const double* p = T.pf_base + (long long)map_row(A, jr) * A.nx + T.pf_col;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(T.pf_bytes) : "memory");
+    }
+}
 
 // x-quantities of a neighbour column re-formed from its ring pairs, with the
 // operations of products() / rhs.hpp:99-109 (bit-identical).
@@ -362,6 +381,7 @@ __device__ __forceinline__ void march_row(const StageArgs& A, const KPtrs& P, Th
     // raw_next may then alias.)
     constexpr bool EARLY = false;
     if (!TMA && EARLY && jn < T.j1) load_raw<MODE>(P, (unsigned)map_row(A, jn + 1) * nx + T.col, raw_next);
+    if (!TMA && HSGN_L2_PF > 1 && jn + HSGN_L2_PF <= T.j1) l2_prefetch_row<MODE>(A, T, jn + HSGN_L2_PF);
     if (TMA) {  // raw row jn lives in raw slot (SC+2)%3; row j+3 goes into slot (SC+1)%3
         constexpr int RS = (SC + 2) % 3, RI = (SC + 1) % 3;
         mbar_wait(&bars[RS], (unsigned)(((jn - j0 + 1) / 3) & 1));
@@ -554,6 +574,19 @@ __global__ void __launch_bounds__(BX, min_blocks<MODE>()) sgn_stage_kernel(const
     T.my_min = ~0ull;
     T.my_err = 0.0;
     const unsigned unx = (unsigned)nx;
+    T.pf_base = nullptr;
+    T.pf_bytes = 0;
+    T.pf_col = 0;
+    if (!TMA && HSGN_L2_PF > 1 && (nx % 2) == 0 && tid < nraw<MODE>()) {
+#pragma unroll
+        for (int f = 0; f < nraw<MODE>(); ++f)
+            if (tid == f)
+                T.pf_base = f < 5 ? P.y[f] : (f == nraw<MODE>() - 1 ? P.b : (f < 10 ? P.k[f - 5] : P.kc[f - 10]));
+        const int a = max((int)blockIdx.x * WX - 2, 0), e = min((int)blockIdx.x * WX + BX, nx);
+        T.pf_col = a;
+        T.pf_bytes = (e - a) * 8;
+        for (int r = j0 + 2; r <= min(j0 + HSGN_L2_PF, T.j1); ++r) l2_prefetch_row<MODE>(A, T, r);
+    }
 
     // ---- prologue: row j0-1 -> register set C (ring slot 2), row j0 -> set A (slot 0)
     YQ ya, yb, yc;
