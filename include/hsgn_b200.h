@@ -191,6 +191,31 @@ double hsgn_outer_sum(const hsgn_grid* grid, const double* rows, int32_t j_begin
 hsgn_status hsgn_profile_stages(hsgn_ctx* ctx, const hsgn_state* y, const hsgn_state* k1, double dt,
                                 int32_t reps, double* ms3);
 
+/* ------------------------------------------------------------ in-process slab group */
+
+/* The y-slab decomposition driven from ONE process:
+ * n slab contexts on devices[r] (NULL: current device; several slabs may
+ * share a GPU), halo rows pulled from the neighbours' boundary rows through
+ * (peer) device pointers after every stage, ordered by CUDA events.  Same
+ * arithmetic and exchange schedule as the NCCL path; host arrays are the
+ * FULL grid. */
+typedef struct hsgn_group hsgn_group;
+typedef struct hsgn_gstate hsgn_gstate;
+hsgn_status hsgn_group_create(const hsgn_grid* grid, const hsgn_phys* phys, const double* b_full,
+                              const int* devices, int32_t n, hsgn_group** out);
+hsgn_status hsgn_group_destroy(hsgn_group* g);
+const char* hsgn_group_last_error(const hsgn_group* g);
+hsgn_status hsgn_group_state_alloc(hsgn_group* g, hsgn_gstate** out);
+hsgn_status hsgn_group_state_free(hsgn_group* g, hsgn_gstate* s);
+hsgn_status hsgn_group_state_upload(hsgn_group* g, hsgn_gstate* s, const double* host_full);
+hsgn_status hsgn_group_state_download(hsgn_group* g, const hsgn_gstate* s, double* host_full);
+hsgn_status hsgn_group_rhs(hsgn_group* g, double t, const hsgn_gstate* q, hsgn_gstate* out, int64_t* bad_nodes);
+hsgn_status hsgn_group_bs3_fixed_steps(hsgn_group* g, hsgn_gstate* y, hsgn_gstate* k1, double t, double dt,
+                                       int64_t steps, int64_t* steps_done);
+/* kind: 0 total mass, 1 total energy, 2 energy rate (q_t required) */
+hsgn_status hsgn_group_reduce(hsgn_group* g, int32_t kind, const hsgn_gstate* q, const hsgn_gstate* q_t,
+                              double* out);
+
 /* ------------------------------------------------------------ misc */
 hsgn_status hsgn_synchronize(hsgn_ctx* ctx);
 /* Elapsed ms of the last hsgn_bs3_fixed_steps call measured with CUDA events

@@ -100,6 +100,17 @@ def lib() -> C.CDLL:
     f("hsgn_last_timing", C.c_int, CTX, PD, C.POINTER(I64))
     f("hsgn_build_info", C.c_char_p)
     f("hsgn_profile_stages", C.c_int, CTX, STATE, STATE, D, I32, PD)
+    GRP, GST = C.c_void_p, C.c_void_p
+    f("hsgn_group_create", C.c_int, G, PH, PD, C.POINTER(C.c_int), I32, C.POINTER(GRP))
+    f("hsgn_group_destroy", C.c_int, GRP)
+    f("hsgn_group_last_error", C.c_char_p, GRP)
+    f("hsgn_group_state_alloc", C.c_int, GRP, C.POINTER(GST))
+    f("hsgn_group_state_free", C.c_int, GRP, GST)
+    f("hsgn_group_state_upload", C.c_int, GRP, GST, PD)
+    f("hsgn_group_state_download", C.c_int, GRP, GST, PD)
+    f("hsgn_group_rhs", C.c_int, GRP, D, GST, GST, C.POINTER(I64))
+    f("hsgn_group_bs3_fixed_steps", C.c_int, GRP, GST, GST, D, D, I64, C.POINTER(I64))
+    f("hsgn_group_reduce", C.c_int, GRP, I32, GST, GST, PD)
     _lib = L
     return L
 
@@ -114,4 +125,7 @@ EXPORTS = [
     "hsgn_bs3_fixed_steps", "hsgn_total_mass", "hsgn_total_energy", "hsgn_energy_rate",
     "hsgn_mass_weighted_sum", "hsgn_discrete_l2_error", "hsgn_row_sums", "hsgn_outer_sum",
     "hsgn_synchronize", "hsgn_last_timing", "hsgn_build_info", "hsgn_profile_stages",
+    "hsgn_group_create", "hsgn_group_destroy", "hsgn_group_last_error", "hsgn_group_state_alloc",
+    "hsgn_group_state_free", "hsgn_group_state_upload", "hsgn_group_state_download", "hsgn_group_rhs",
+    "hsgn_group_bs3_fixed_steps", "hsgn_group_reduce",
 ]

@@ -127,6 +127,7 @@ struct hsgn_ctx {
     int rows_per_block = 0;
     int forced_kind = -1;  // stencil kind override (tests); -1 = automatic
     int use_tma = 0;       // TMA staging of raw inputs when nx is even (opt-in: slower in r1)
+    int in_group = 0;      // member of an in-process slab group (halo pulls by the group)
     int64_t n_evals = 0;
     std::string err;
     // workspace for the integrator
@@ -286,7 +287,7 @@ static hsgn_status setup_ctx(hsgn_ctx* c) {
 // receive into our rows -1 / ny_loc.  One grouped NCCL call per exchange, on
 // the context stream (graph-capturable).
 static hsgn_status exchange(hsgn_ctx* c, const hsgn_state* s, int nfields) {
-    if (c->nranks == 1) return HSGN_OK;
+    if (c->nranks == 1 || c->in_group) return HSGN_OK;  // in a group the driver pulls halos
     if (!c->comm) return fail(c, HSGN_ENCCL, "slab context has no NCCL communicator attached");
     const NcclApi& N = nccl();
     const int nx = c->grid.nx;
@@ -367,23 +368,42 @@ static void reset_recs(hsgn_ctx* c, int n) {
 // Enqueue one fused BS3 step (S1, S2, S3 + halo exchanges) on the stream.
 //   y, k1 : step inputs;  ynew, k4 : outputs;  k2 : scratch;  rec : this step's record
 //   prev  : previous step's record (halt check) or null
-static hsgn_status enqueue_step(hsgn_ctx* c, const hsgn_state* y, const hsgn_state* k1, hsgn_state* k2,
-                                hsgn_state* ynew, hsgn_state* k4, hsgn_state* part, StepRec* rec,
-                                const StepRec* prev, double t, double dt, bool adaptive, double atol,
-                                double rtol, int64_t* kernels) {
-    hsgn_status s;
-    // stage 1: k2 = f(t + dt/2, y + (dt/2) k1)
-    StageArgs A = stage_args(c, MODE_S1, t + 0.5 * dt);
-    A.a = 0.5 * dt;
-    A.y = y->base;
-    A.k = k1->base;
-    A.out = k2->base;
-    A.bad = &rec->bad[0];
-    A.halt = c->d_halt;
-    A.chk_bad = prev ? &prev->bad[2] : nullptr;
-    A.chk_minh = prev ? &prev->minh : nullptr;
-    if ((s = launch(c, MODE_S1, A))) return s;
-    if ((s = exchange(c, k2, 5))) return s;
+// One stage kernel of a fused BS3 step (stage = 1, 2, 3), without the halo
+// exchange of its output (k2, ynew, k4 respectively).
+static hsgn_status enqueue_stage(hsgn_ctx* c, int stage, const hsgn_state* y, const hsgn_state* k1, hsgn_state* k2,
+                                 hsgn_state* ynew, hsgn_state* k4, hsgn_state* part, StepRec* rec,
+                                 const StepRec* prev, double t, double dt, bool adaptive, double atol,
+                                 double rtol) {
+    StageArgs A;
+    if (stage == 1) {  // k2 = f(t + dt/2, y + (dt/2) k1)
+        A = stage_args(c, MODE_S1, t + 0.5 * dt);
+        A.a = 0.5 * dt;
+        A.y = y->base;
+        A.k = k1->base;
+        A.out = k2->base;
+        A.bad = &rec->bad[0];
+        A.halt = c->d_halt;
+        A.chk_bad = prev ? &prev->bad[2] : nullptr;
+        A.chk_minh = prev ? &prev->minh : nullptr;
+        return launch(c, MODE_S1, A);
+    }
+    if (stage == 3) {  // k4 = f(t + dt, ynew) (FSAL)
+        A = stage_args(c, MODE_S3, t + dt);
+        A.y = ynew->base;
+        A.out = k4->base;
+        A.adaptive = adaptive;
+        A.d4 = -1.0 / 8.0;
+        A.dt = dt;
+        A.atol = atol;
+        A.rtol = rtol;
+        A.part = part ? part->base : nullptr;
+        A.yold = y->base;
+        A.err_part = c->d_err_part;
+        A.bad = &rec->bad[2];
+        A.halt = c->d_halt;
+        A.chk_bad = &rec->bad[1];
+        return launch(c, MODE_S3, A);
+    }
     // stage 2: k3 = f(t + 3dt/4, y + (3dt/4) k2); ynew = y + (2/9 dt) k1 + (1/3 dt) k2 + (4/9 dt) k3
     A = stage_args(c, MODE_S2, t + 0.75 * dt);
     A.a = 0.75 * dt;
@@ -404,25 +424,21 @@ static hsgn_status enqueue_step(hsgn_ctx* c, const hsgn_state* y, const hsgn_sta
     A.minh = &rec->minh;
     A.halt = c->d_halt;
     A.chk_bad = &rec->bad[0];
-    if ((s = launch(c, MODE_S2, A))) return s;
-    if ((s = exchange(c, ynew, 5))) return s;
-    // stage 3: k4 = f(t + dt, ynew) (FSAL)
-    A = stage_args(c, MODE_S3, t + dt);
-    A.y = ynew->base;
-    A.out = k4->base;
-    A.adaptive = adaptive;
-    A.d4 = -1.0 / 8.0;
-    A.dt = dt;
-    A.atol = atol;
-    A.rtol = rtol;
-    A.part = part ? part->base : nullptr;
-    A.yold = y->base;
-    A.err_part = c->d_err_part;
-    A.bad = &rec->bad[2];
-    A.halt = c->d_halt;
-    A.chk_bad = &rec->bad[1];
-    if ((s = launch(c, MODE_S3, A))) return s;
-    if ((s = exchange(c, k4, 5))) return s;
+    return launch(c, MODE_S2, A);
+}
+
+// One fused BS3 step (S1, S2, S3) with the slab halo exchange after each
+// stage (k2, ynew, k4): DESIGN.md section 6.
+static hsgn_status enqueue_step(hsgn_ctx* c, const hsgn_state* y, const hsgn_state* k1, hsgn_state* k2,
+                                hsgn_state* ynew, hsgn_state* k4, hsgn_state* part, StepRec* rec,
+                                const StepRec* prev, double t, double dt, bool adaptive, double atol,
+                                double rtol, int64_t* kernels) {
+    hsgn_state* produced[3] = {k2, ynew, k4};
+    for (int stage = 1; stage <= 3; ++stage) {
+        hsgn_status s = enqueue_stage(c, stage, y, k1, k2, ynew, k4, part, rec, prev, t, dt, adaptive, atol, rtol);
+        if (s) return s;
+        if ((s = exchange(c, produced[stage - 1], 5))) return s;
+    }
     if (kernels) *kernels += 3;
     return HSGN_OK;
 }
@@ -1280,3 +1296,353 @@ extern "C" hsgn_status hsgn_profile_stages(hsgn_ctx* c, const hsgn_state* y, con
     for (int k = 0; k < 3; ++k) ms3[k] = acc[k] / reps;
     return HSGN_OK;
 }
+
+// ------------------------------------------------------------------ in-process slab group
+// The slab decomposition of DESIGN.md section 6 driven from ONE process: N
+// slab contexts (on one or several devices) whose halo rows move by a pull
+// kernel reading the neighbours' boundary rows through (peer) device
+// pointers, ordered by CUDA events -- no spinning, so several slabs may share
+// one GPU.  Used to test the multi-slab kernel path on a single B200, and as
+// a single-process multi-GPU transport (NVLink peer reads).
+
+struct hsgn_group {
+    hsgn_grid grid{};
+    int n = 0;
+    std::vector<hsgn_ctx*> m;
+    std::vector<int> j0, j1;
+    std::vector<cudaEvent_t> evk, evp;  // per member: stage kernel done / halo pull done
+    std::string err;
+};
+
+struct hsgn_gstate {
+    std::vector<hsgn_state*> p;
+};
+
+namespace {
+
+struct HaloPull {
+    double* dst[10];
+    const double* src[10];
+    int nx, count;
+};
+
+__global__ void halo_pull_kernel(const HaloPull H) {
+    const int k = blockIdx.y;
+    if (k >= H.count) return;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < H.nx; i += gridDim.x * blockDim.x) H.dst[k][i] = H.src[k][i];
+}
+
+int g_dn(const hsgn_group* G, int r) {
+    if (r > 0) return r - 1;
+    return G->grid.kind_y == HSGN_BOUNDED ? -1 : G->n - 1;
+}
+int g_up(const hsgn_group* G, int r) {
+    if (r + 1 < G->n) return r + 1;
+    return G->grid.kind_y == HSGN_BOUNDED ? -1 : 0;
+}
+
+hsgn_status gfail(hsgn_group* G, hsgn_status s, const std::string& what) {
+    G->err = what;
+    return s;
+}
+
+// Fill the ghost rows of every member's part of `parts` (nf fields) from its
+// neighbours, after their latest kernels (evk); record evp.
+hsgn_status group_pull(hsgn_group* G, const std::vector<hsgn_state*>& parts, int nf) {
+    for (int r = 0; r < G->n; ++r) {
+        hsgn_ctx* c = G->m[r];
+        const int dn = g_dn(G, r), up = g_up(G, r);
+        cudaSetDevice(c->device);
+        HaloPull H;
+        H.nx = G->grid.nx;
+        H.count = 0;
+        const long long nx = G->grid.nx;
+        for (int f = 0; f < nf; ++f) {
+            if (dn >= 0) {
+                const hsgn_ctx* d = G->m[dn];
+                H.dst[H.count] = parts[r]->f(f) - nx;
+                H.src[H.count] = parts[dn]->f(f) + (long long)(d->ny_loc - 1) * nx;
+                ++H.count;
+            }
+            if (up >= 0) {
+                H.dst[H.count] = parts[r]->f(f) + (long long)c->ny_loc * nx;
+                H.src[H.count] = parts[up]->f(f);
+                ++H.count;
+            }
+        }
+        if (dn >= 0) cudaStreamWaitEvent(c->stream, G->evk[dn], 0);
+        if (up >= 0) cudaStreamWaitEvent(c->stream, G->evk[up], 0);
+        if (H.count) halo_pull_kernel<<<dim3((H.nx + 255) / 256 < 64 ? (H.nx + 255) / 256 : 64, H.count), 256, 0,
+                                        c->stream>>>(H);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return gfail(G, HSGN_ECUDA, cudaGetErrorString(e));
+        cudaEventRecord(G->evp[r], c->stream);
+    }
+    return HSGN_OK;
+}
+
+// Before a member overwrites buffers its neighbours may still be reading.
+void group_wait_pulls(hsgn_group* G, int r) {
+    const int dn = g_dn(G, r), up = g_up(G, r);
+    hsgn_ctx* c = G->m[r];
+    if (dn >= 0) cudaStreamWaitEvent(c->stream, G->evp[dn], 0);
+    if (up >= 0) cudaStreamWaitEvent(c->stream, G->evp[up], 0);
+}
+
+}  // namespace
+
+extern "C" {
+
+hsgn_status hsgn_group_create(const hsgn_grid* grid, const hsgn_phys* phys, const double* b_full, const int* devices,
+                              int32_t n, hsgn_group** out) {
+    if (!grid || !phys || !b_full || !out || n < 1 || grid->ny < 2 * n) return HSGN_EINVAL;
+    hsgn_group* G = new hsgn_group();
+    G->grid = *grid;
+    G->n = n;
+    const int base = grid->ny / n, rem = grid->ny % n;  // slab.py partition(): first ranks take the remainder
+    int j = 0;
+    for (int r = 0; r < n; ++r) {
+        const int k = base + (r < rem ? 1 : 0);
+        G->j0.push_back(j);
+        G->j1.push_back(j + k);
+        j += k;
+    }
+    for (int r = 0; r < n; ++r) {
+        hsgn_ctx* c = nullptr;
+        const int dev = devices ? devices[r] : -1;
+        hsgn_status s = hsgn_ctx_create_slab(grid, phys, b_full + (long long)G->j0[r] * grid->nx, dev, G->j0[r],
+                                             G->j1[r], r, n, &c);
+        if (s) {
+            hsgn_group_destroy(G);
+            return s;
+        }
+        c->in_group = 1;
+        G->m.push_back(c);
+        cudaEvent_t a, b;
+        cudaSetDevice(c->device);
+        cudaEventCreateWithFlags(&a, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&b, cudaEventDisableTiming);
+        G->evk.push_back(a);
+        G->evp.push_back(b);
+    }
+    for (int r = 0; r < n; ++r)  // peer access between neighbouring devices (no-op on one device)
+        for (int q : {g_dn(G, r), g_up(G, r)})
+            if (q >= 0 && G->m[q]->device != G->m[r]->device) {
+                cudaSetDevice(G->m[r]->device);
+                cudaDeviceEnablePeerAccess(G->m[q]->device, 0);
+                cudaGetLastError();
+            }
+    // bathymetry ghost rows (static field, one pull)
+    std::vector<hsgn_state*> bs(n);
+    std::vector<hsgn_state> bstore(n);
+    for (int r = 0; r < n; ++r) {
+        bstore[r].base = G->m[r]->b;
+        bstore[r].fs = G->m[r]->fs;
+        bs[r] = &bstore[r];
+        cudaSetDevice(G->m[r]->device);
+        cudaStreamSynchronize(G->m[r]->stream);
+        cudaEventRecord(G->evk[r], G->m[r]->stream);
+    }
+    hsgn_status s = group_pull(G, bs, 1);
+    for (int r = 0; r < n; ++r) cudaStreamSynchronize(G->m[r]->stream);
+    if (s) {
+        hsgn_group_destroy(G);
+        return s;
+    }
+    *out = G;
+    return HSGN_OK;
+}
+
+hsgn_status hsgn_group_destroy(hsgn_group* G) {
+    if (!G) return HSGN_OK;
+    for (int r = 0; r < (int)G->m.size(); ++r) {
+        cudaSetDevice(G->m[r]->device);
+        if (r < (int)G->evk.size()) cudaEventDestroy(G->evk[r]);
+        if (r < (int)G->evp.size()) cudaEventDestroy(G->evp[r]);
+        hsgn_ctx_destroy(G->m[r]);
+    }
+    delete G;
+    return HSGN_OK;
+}
+
+const char* hsgn_group_last_error(const hsgn_group* G) { return G ? G->err.c_str() : "null group"; }
+
+hsgn_status hsgn_group_state_alloc(hsgn_group* G, hsgn_gstate** out) {
+    if (!G || !out) return HSGN_EINVAL;
+    hsgn_gstate* s = new hsgn_gstate();
+    for (hsgn_ctx* c : G->m) {
+        hsgn_state* p = nullptr;
+        hsgn_status st = hsgn_state_alloc(c, &p);
+        if (st) {
+            hsgn_group_state_free(G, s);
+            return st;
+        }
+        s->p.push_back(p);
+    }
+    *out = s;
+    return HSGN_OK;
+}
+
+hsgn_status hsgn_group_state_free(hsgn_group* G, hsgn_gstate* s) {
+    if (!G || !s) return HSGN_EINVAL;
+    for (size_t r = 0; r < s->p.size(); ++r) hsgn_state_free(G->m[r], s->p[r]);
+    delete s;
+    return HSGN_OK;
+}
+
+// host layout: the full grid (5 fields of nx*ny); each member takes its rows
+hsgn_status hsgn_group_state_upload(hsgn_group* G, hsgn_gstate* s, const double* host) {
+    if (!G || !s || !host) return HSGN_EINVAL;
+    const long long nx = G->grid.nx, n = nx * G->grid.ny;
+    for (int r = 0; r < G->n; ++r) {
+        hsgn_ctx* c = G->m[r];
+        cudaSetDevice(c->device);
+        for (int f = 0; f < 5; ++f)
+            if (cudaMemcpyAsync(s->p[r]->f(f), host + f * n + G->j0[r] * nx, sizeof(double) * nx * c->ny_loc,
+                                cudaMemcpyHostToDevice, c->stream) != cudaSuccess)
+                return gfail(G, HSGN_ECUDA, "upload");
+        group_wait_pulls(G, r);
+        cudaEventRecord(G->evk[r], c->stream);
+    }
+    hsgn_status st = group_pull(G, s->p, 5);
+    for (hsgn_ctx* c : G->m) cudaStreamSynchronize(c->stream);
+    return st;
+}
+
+hsgn_status hsgn_group_state_download(hsgn_group* G, const hsgn_gstate* s, double* host) {
+    if (!G || !s || !host) return HSGN_EINVAL;
+    const long long nx = G->grid.nx, n = nx * G->grid.ny;
+    for (int r = 0; r < G->n; ++r) {
+        hsgn_ctx* c = G->m[r];
+        cudaSetDevice(c->device);
+        for (int f = 0; f < 5; ++f) {
+            const cudaError_t e = cudaMemcpyAsync(host + f * n + G->j0[r] * nx, s->p[r]->f(f),
+                                                  sizeof(double) * nx * c->ny_loc, cudaMemcpyDeviceToHost, c->stream);
+            if (e != cudaSuccess) return gfail(G, HSGN_ECUDA, std::string("download: ") + cudaGetErrorString(e));
+        }
+    }
+    for (hsgn_ctx* c : G->m) cudaStreamSynchronize(c->stream);
+    return HSGN_OK;
+}
+
+// rhs on the decomposed grid (ghost rows of q must be current: upload does it)
+hsgn_status hsgn_group_rhs(hsgn_group* G, double t, const hsgn_gstate* q, hsgn_gstate* out, int64_t* bad_nodes) {
+    if (!G || !q || !out) return HSGN_EINVAL;
+    int64_t bad = 0;
+    for (int r = 0; r < G->n; ++r) {
+        hsgn_ctx* c = G->m[r];
+        cudaSetDevice(c->device);
+        hsgn_status s = ensure_recs(c, 1);
+        if (s) return s;
+        cudaMemsetAsync(&c->d_rec[0].bad[0], 0, sizeof(unsigned long long), c->stream);
+        group_wait_pulls(G, r);
+        if ((s = rhs_raw(c, t, q->p[r], out->p[r], 0.0, false, &c->d_rec[0].bad[0]))) return s;
+        cudaEventRecord(G->evk[r], c->stream);
+    }
+    hsgn_status s = group_pull(G, out->p, 5);
+    if (s) return s;
+    for (int r = 0; r < G->n; ++r) {
+        hsgn_ctx* c = G->m[r];
+        unsigned long long hb = 0;
+        cudaMemcpyAsync(&hb, &c->d_rec[0].bad[0], sizeof hb, cudaMemcpyDeviceToHost, c->stream);
+        cudaStreamSynchronize(c->stream);
+        bad += (int64_t)hb;
+    }
+    if (bad_nodes) *bad_nodes = bad;
+    return bad ? gfail(G, HSGN_EDEPTH, "non-positive depth") : HSGN_OK;
+}
+
+// `steps` fused fixed-step BS3 steps on (y, k1) in place, halo pulls after
+// every stage (the NCCL schedule of enqueue_step with an in-process transport)
+hsgn_status hsgn_group_bs3_fixed_steps(hsgn_group* G, hsgn_gstate* y, hsgn_gstate* k1, double t, double dt,
+                                       int64_t steps, int64_t* steps_done) {
+    if (!G || !y || !k1 || steps < 0) return HSGN_EINVAL;
+    const int n = G->n;
+    for (hsgn_ctx* c : G->m) {
+        cudaSetDevice(c->device);
+        hsgn_status s = ensure_ws(c, 1);
+        if (s) return s;
+    }
+    // work in each member's workspace: y -> ws[0], k1 -> ws[2]
+    std::vector<hsgn_state*> Y[2], K[2], K2(n);
+    for (int r = 0; r < n; ++r) {
+        hsgn_ctx* c = G->m[r];
+        Y[0].push_back(&c->ws[0]);
+        Y[1].push_back(&c->ws[1]);
+        K[0].push_back(&c->ws[2]);
+        K[1].push_back(&c->ws[3]);
+        K2[r] = &c->ws[4];
+        cudaSetDevice(c->device);
+        group_wait_pulls(G, r);
+        cudaMemcpyAsync(c->ws[0].base - c->grid.nx, y->p[r]->base - c->grid.nx, sizeof(double) * 5 * c->fs,
+                        cudaMemcpyDeviceToDevice, c->stream);
+        cudaMemcpyAsync(c->ws[2].base - c->grid.nx, k1->p[r]->base - c->grid.nx, sizeof(double) * 5 * c->fs,
+                        cudaMemcpyDeviceToDevice, c->stream);
+        cudaEventRecord(G->evk[r], c->stream);
+        cudaEventRecord(G->evp[r], c->stream);
+    }
+    int p = 0;
+    int64_t done = 0;
+    hsgn_status result = HSGN_OK;
+    for (int64_t step = 0; step < steps; ++step) {
+        for (int stage = 1; stage <= 3; ++stage) {
+            for (int r = 0; r < n; ++r) {
+                hsgn_ctx* c = G->m[r];
+                cudaSetDevice(c->device);
+                if (stage == 1) reset_recs(c, 1);
+                group_wait_pulls(G, r);
+                hsgn_status s = enqueue_stage(c, stage, Y[p][r], K[p][r], K2[r], Y[p ^ 1][r], K[p ^ 1][r], nullptr,
+                                              &c->d_rec[0], nullptr, t, dt, false, 0, 0);
+                if (s) return s;
+                cudaEventRecord(G->evk[r], c->stream);
+            }
+            const std::vector<hsgn_state*>& produced = stage == 1 ? K2 : (stage == 2 ? Y[p ^ 1] : K[p ^ 1]);
+            hsgn_status s = group_pull(G, produced, 5);
+            if (s) return s;
+        }
+        bool bad = false;
+        for (int r = 0; r < n; ++r) {
+            hsgn_ctx* c = G->m[r];
+            StepRec rec;
+            cudaSetDevice(c->device);
+            cudaMemcpyAsync(&rec, &c->d_rec[0], sizeof rec, cudaMemcpyDeviceToHost, c->stream);
+            cudaStreamSynchronize(c->stream);
+            bad |= (rec.bad[0] | rec.bad[1] | rec.bad[2]) != 0;
+            c->n_evals += 3;
+        }
+        if (bad) {
+            result = gfail(G, HSGN_EDEPTH, "non-positive depth in fixed-step mode");
+            break;
+        }
+        t = t + dt;
+        p ^= 1;
+        ++done;
+    }
+    for (int r = 0; r < n; ++r) {
+        hsgn_ctx* c = G->m[r];
+        cudaSetDevice(c->device);
+        cudaMemcpyAsync(y->p[r]->base - c->grid.nx, Y[p][r]->base - c->grid.nx, sizeof(double) * 5 * c->fs,
+                        cudaMemcpyDeviceToDevice, c->stream);
+        cudaMemcpyAsync(k1->p[r]->base - c->grid.nx, K[p][r]->base - c->grid.nx, sizeof(double) * 5 * c->fs,
+                        cudaMemcpyDeviceToDevice, c->stream);
+        cudaStreamSynchronize(c->stream);
+    }
+    if (steps_done) *steps_done = done;
+    return result;
+}
+
+// Decomposition-independent SBP-norm totals: per-slab row sums gathered in
+// global row order, one outer sum (kind: 0 mass, 1 energy, 2 energy rate).
+hsgn_status hsgn_group_reduce(hsgn_group* G, int32_t kind, const hsgn_gstate* q, const hsgn_gstate* qt,
+                              double* out) {
+    if (!G || !q || !out || kind < 0 || kind > 2 || (kind == 2 && !qt)) return HSGN_EINVAL;
+    std::vector<double> rows(G->grid.ny);
+    for (int r = 0; r < G->n; ++r) {
+        hsgn_status s = hsgn_row_sums(G->m[r], kind, q->p[r], qt ? qt->p[r] : nullptr, 0, rows.data() + G->j0[r]);
+        if (s) return s;
+    }
+    *out = outer_sum(&G->grid, rows.data(), 0, G->grid.ny);
+    return HSGN_OK;
+}
+
+}  // extern "C"

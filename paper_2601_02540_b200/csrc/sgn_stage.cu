@@ -69,11 +69,13 @@ struct YQ {  // y-differentiated quantities of one row at this column (rhs.hpp:1
     double h, u, v, w, e, hhb, v2, hv, huv, e2h, hvw, b;
 };
 
-// Memory row index of logical row jr (may be -1 or ny) of the slab.
+// Memory row of logical row jr (may be -1 or ny) of the slab, counted from
+// the ghost row -1 (every KPtrs base points at row -1, so offsets stay
+// non-negative 32-bit values even for the lower ghost row).
 __device__ __forceinline__ int map_row(const StageArgs& A, int jr) {
-    if (jr < 0) return A.y_lo == YE_WRAP ? A.ny - 1 : (A.y_lo == YE_CLAMP ? 0 : -1);
-    if (jr >= A.ny) return A.y_hi == YE_WRAP ? 0 : (A.y_hi == YE_CLAMP ? A.ny - 1 : A.ny);
-    return jr;
+    if (jr < 0) return A.y_lo == YE_WRAP ? A.ny : (A.y_lo == YE_CLAMP ? 1 : 0);
+    if (jr >= A.ny) return A.y_hi == YE_WRAP ? 1 : (A.y_hi == YE_CLAMP ? A.ny : A.ny + 1);
+    return jr + 1;
 }
 
 template <int MODE>
@@ -500,7 +502,7 @@ __device__ __forceinline__ void march_row(const StageArgs& A, const KPtrs& P, Th
         for (int f = 0; f < 5; ++f) o[f] = dadd(o[f], s5[f]);
     }
     // ---- epilogue
-    const unsigned off = (unsigned)j * nx + T.col;
+    const unsigned off = (unsigned)(j + 1) * nx + T.col;  // bases point at row -1
     if (MODE == MODE_S2) {
         const double2 y01 = Sc[P_YP01 * BX], y23 = Sc[P_YP23 * BX], y4 = Sc[P_YP4 * BX];
         const double ypart[5] = {y01.x, y01.y, y23.x, y23.y, y4.x};
@@ -514,12 +516,14 @@ __device__ __forceinline__ void march_row(const StageArgs& A, const KPtrs& P, Th
             }
         }
         if (A.adaptive)
-            s2_error_partial(A.kc, A.k, A.part, A.fs, off, A.d1, A.d2, A.d3, o[0], o[1], o[2], o[3], o[4]);
+            s2_error_partial(A.kc - A.nx, A.k - A.nx, A.part - A.nx, A.fs, off, A.d1, A.d2, A.d3, o[0], o[1], o[2],
+                             o[3], o[4]);
     } else {
 #pragma unroll
         for (int f = 0; f < 5; ++f) P.out[f][off] = o[f];
         if (MODE == MODE_S3 && A.adaptive)
-            T.my_err = dadd(T.my_err, s3_error_sq(A.part, A.yold, A.y, A.fs, off, A.dt, A.d4, A.atol, A.rtol, o[0],
+            T.my_err = dadd(T.my_err, s3_error_sq(A.part - A.nx, A.yold - A.nx, A.y - A.nx, A.fs, off, A.dt, A.d4,
+                                                  A.atol, A.rtol, o[0],
                                                   o[1], o[2], o[3], o[4]));
     }
 }
@@ -613,7 +617,7 @@ __global__ void __launch_bounds__(BX, min_blocks<MODE>()) sgn_stage_kernel(const
         mbar_wait(&bars[1], 0);
         raw_from_smem<MODE>(rawring + nraw<MODE>() * RW, tid, raw);
     } else {
-        load_raw<MODE>(P, (unsigned)j0 * unx + T.col, raw);
+        load_raw<MODE>(P, (unsigned)(j0 + 1) * unx + T.col, raw);
     }
     {
         const bool ok = products<MODE>(A, raw, ring + tid, ya);
@@ -712,16 +716,17 @@ static cudaError_t launch_tma(const StageArgs& A, const KPtrs& P, cudaStream_t s
 
 template <int MODE, int KIND>
 static cudaError_t launch_mode(const StageArgs& A, cudaStream_t st) {
-    KPtrs P;
+    KPtrs P;  // field bases at the ghost row -1 (see map_row)
+    const long long g = A.nx;
     for (int f = 0; f < 5; ++f) {
-        P.y[f] = A.y ? A.y + f * A.fs : nullptr;
-        P.k[f] = A.k ? A.k + f * A.fs : nullptr;
-        P.kc[f] = A.kc ? A.kc + f * A.fs : nullptr;
-        P.out[f] = A.out ? A.out + f * A.fs : nullptr;
-        P.part[f] = A.part ? A.part + f * A.fs : nullptr;
-        P.yold[f] = A.yold ? A.yold + f * A.fs : nullptr;
+        P.y[f] = A.y ? A.y + f * A.fs - g : nullptr;
+        P.k[f] = A.k ? A.k + f * A.fs - g : nullptr;
+        P.kc[f] = A.kc ? A.kc + f * A.fs - g : nullptr;
+        P.out[f] = A.out ? A.out + f * A.fs - g : nullptr;
+        P.part[f] = A.part ? A.part + f * A.fs - g : nullptr;
+        P.yold[f] = A.yold ? A.yold + f * A.fs - g : nullptr;
     }
-    P.b = A.b;
+    P.b = A.b - g;
     // TMA staging needs 16-byte aligned row pieces: nx even (host decides)
     if (A.tma && (A.nx % 2) == 0) return launch_tma<MODE, KIND, true>(A, P, st);
     return launch_tma<MODE, KIND, false>(A, P, st);

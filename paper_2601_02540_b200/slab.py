@@ -64,6 +64,73 @@ def slab_fields(nx: int, ny: int, t: float, rank: int, nranks: int):
     return g, q, b
 
 
+class SlabGroup:
+    """In-process slab decomposition (hsgn_group_*): n slabs on `devices`
+    (default: all on the current device), halo rows pulled over (peer)
+    device pointers after every stage.  Host arrays are the full grid."""
+
+    def __init__(self, grid, phys, n: int, devices=None):
+        from . import _native as N
+        self.N = N
+        self.grid, self.n = grid, n
+        b = np.ascontiguousarray(phys.b if phys.b is not None else np.zeros((grid.ny, grid.nx)), dtype=np.float64)
+        g = grid.c_struct()
+        ph = N.hsgn_phys(phys.g, phys.lambda_, phys.h_floor)
+        devs = (C.c_int * n)(*(devices or [-1] * n))
+        self._h = C.c_void_p()
+        st = N.lib().hsgn_group_create(C.byref(g), C.byref(ph), b.ctypes.data_as(N.PD), devs, n, C.byref(self._h))
+        if st:
+            raise RuntimeError(f"hsgn_group_create failed ({st})")
+        self.rows = partition(grid.ny, n)
+
+    def _check(self, st, what):
+        if st:
+            msg = self.N.lib().hsgn_group_last_error(self._h)
+            raise RuntimeError(f"{what}: status {st} {msg.decode() if msg else ''}")
+
+    def state(self, host=None):
+        s = C.c_void_p()
+        self._check(self.N.lib().hsgn_group_state_alloc(self._h, C.byref(s)), "state_alloc")
+        if host is not None:
+            self.upload(s, host)
+        return s
+
+    def upload(self, s, host):
+        a = np.ascontiguousarray(host, dtype=np.float64).reshape(-1)
+        self._check(self.N.lib().hsgn_group_state_upload(self._h, s, a.ctypes.data_as(self.N.PD)), "upload")
+
+    def download(self, s):
+        out = np.empty(5 * self.grid.nx * self.grid.ny)
+        self._check(self.N.lib().hsgn_group_state_download(self._h, s, out.ctypes.data_as(self.N.PD)), "download")
+        return out
+
+    def rhs(self, t, q, out):
+        bad = C.c_int64(0)
+        self._check(self.N.lib().hsgn_group_rhs(self._h, float(t), q, out, C.byref(bad)), "rhs")
+
+    def bs3_fixed_steps(self, y, k1, t, dt, steps):
+        done = C.c_int64(0)
+        self._check(self.N.lib().hsgn_group_bs3_fixed_steps(self._h, y, k1, float(t), float(dt), int(steps),
+                                                             C.byref(done)), "bs3_fixed_steps")
+        return done.value
+
+    def reduce(self, kind, q, qt=None):
+        out = C.c_double(0.0)
+        self._check(self.N.lib().hsgn_group_reduce(self._h, int(kind), q, qt, C.byref(out)), "reduce")
+        return out.value
+
+    def close(self):
+        if self._h:
+            self.N.lib().hsgn_group_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def make_slab_context(grid, phys, rank: int, nranks: int, device: int, dist):
     """Create this rank's slab context and attach an NCCL communicator whose
     unique id is broadcast from rank 0 over torch.distributed."""
