@@ -10,7 +10,9 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_native", "libhsgn_b200.so")
+# HSGN_LIB may point at an alternative in-tree build (A/B measurements of
+# kernel variants in one GPU session); default: the in-tree library.
+LIB_PATH = os.environ.get("HSGN_LIB") or os.path.join(HERE, "_native", "libhsgn_b200.so")
 
 D = C.c_double
 PD = C.POINTER(C.c_double)

@@ -15,7 +15,7 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-OUT_DIR = os.path.join(HERE, "_native")
+OUT_DIR = os.environ.get("HSGN_BUILD_DIR") or os.path.join(HERE, "_native")  # variants: experiments only
 LIB = os.path.join(OUT_DIR, "libhsgn_b200.so")
 SOURCES = ["sgn_stage.cu", "sgn_aux.cu", "hsgn_host.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -46,7 +46,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     log = []
     for src in SOURCES:
         obj = os.path.join(OUT_DIR, src.replace(".cu", ".o"))
-        cmd = [nvcc(), *ARCH, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+        extra = os.environ.get("HSGN_NVCC_EXTRA", "").split()  # experiments only (e.g. -DHSGN_MIN_BLOCKS=4)
+        cmd = [nvcc(), *ARCH, *FLAGS, *extra, "-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         log.append(r.stdout + r.stderr)
         if r.returncode != 0:

@@ -38,13 +38,17 @@ namespace hsgn_dev {
 constexpr int BX = 128;     // threads per CTA == columns touched per tile
 constexpr int WX = BX - 2;  // finished columns per tile
 #ifndef HSGN_MIN_BLOCKS
-#define HSGN_MIN_BLOCKS 3
+#define HSGN_MIN_BLOCKS 0  // 0: per-stage choice in min_blocks()
 #endif
 
 template <int MODE>
 __host__ __device__ constexpr int npairs() { return MODE == MODE_S2 ? NPAIRS_S2 : NPAIRS; }
 template <int MODE>
-__host__ __device__ constexpr int min_blocks() { return HSGN_MIN_BLOCKS; }
+__host__ __device__ constexpr int min_blocks() {
+    // measured (r1): S2 (largest ring, 16 raw inputs) is best at 3 CTAs/SM;
+    // the other stages fit 96 registers without spills and run best at 5
+    return HSGN_MIN_BLOCKS > 0 ? HSGN_MIN_BLOCKS : (MODE == MODE_S2 ? 3 : 5);
+}
 
 // Per-field device pointers (kernel parameters live in the constant bank, so
 // every global address is one IMAD.WIDE of the 32-bit node offset).
@@ -366,6 +370,28 @@ __device__ __forceinline__ void neighbour_x(const double2* S, XQ& X) {
     X.huw = dmul(X.hu, X.w);
 }
 
+#ifndef HSGN_YWIN_SMEM
+#define HSGN_YWIN_SMEM 1
+#endif
+
+// y-quantities of a row re-formed from its own-column ring pairs (same
+// operations as products(), so bit-identical to the carried values).
+__device__ __forceinline__ void neighbour_y(const double2* S, YQ& Y) {
+    const double2 p0 = S[P_HU * BX], p1 = S[P_VW * BX], p2 = S[P_EB * BX], p3 = S[P_RHB * BX];
+    Y.h = p0.x;
+    Y.u = p0.y;
+    Y.v = p1.x;
+    Y.w = p1.y;
+    Y.e = p2.x;
+    Y.b = p2.y;
+    Y.hhb = dmul(Y.h, p3.y);
+    Y.v2 = dmul(Y.v, Y.v);
+    Y.hv = dmul(Y.h, Y.v);
+    Y.huv = dmul(dmul(Y.h, Y.u), Y.v);
+    Y.e2h = dmul(Y.e, p3.x);
+    Y.hvw = dmul(Y.hv, Y.w);
+}
+
 // One row of the march: form row jn = j+1 (ring slot SN, register set yn),
 // then finish row j (ring slot SC; row j-1 is register set yp).
 template <int MODE, int KIND, bool TMA, int SC>
@@ -416,7 +442,15 @@ __device__ __forceinline__ void march_row(const StageArgs& A, const KPtrs& P, Th
     neighbour_x(S + T.sl, L);
     neighbour_x(S + T.sr, R);
 #define DX(f) const double d##f##_x = sbp_d<KIND>(cx, L.f, R.f)
-#define DY(f) const double d##f##_y = sbp_d<KIND>(cy, yp.f, yn.f)
+    // Row j-1: S1/S3/RHS re-form it from its ring entry (slot SP, own
+    // column), which frees the carried window's registers (96 instead of
+    // ~160) for 6 DMUL + 4 LDS.128 per node; S2 keeps the register window
+    // (measured faster for S2, r1: 2.05 vs 2.95 ms).
+    constexpr bool ywin_smem = HSGN_YWIN_SMEM && MODE != MODE_S2;
+    YQ yprev;
+    if (ywin_smem) neighbour_y(ring + ((SC + 2) % 3) * (NP * BX) + T.tid, yprev);
+    const YQ& ypr = ywin_smem ? yprev : yp;
+#define DY(f) const double d##f##_y = sbp_d<KIND>(cy, ypr.f, yn.f)
     DX(h); DX(u); DX(v); DX(w); DX(e); DX(b); DX(hhb); DX(u2); DX(hu); DX(huv); DX(e2h); DX(huw);
     DY(h); DY(u); DY(v); DY(w); DY(e); DY(b); DY(hhb); DY(v2); DY(hv); DY(huv); DY(e2h); DY(hvw);
 #undef DX
@@ -694,8 +728,13 @@ __global__ void __launch_bounds__(256) sum_partials_kernel(const double* part, i
 
 // ----------------------------------------------------------------- launch
 
+__host__ __device__ constexpr size_t cmax(size_t a, size_t b) { return a < b ? b : a; }
+
 template <int MODE, bool TMA>
 __host__ __device__ constexpr size_t ring_bytes() {
+    // (S2 must keep ~80 KB of L1 beside its rings -- 3 CTAs of 49 KB: its 16
+    // misaligned raw streams rely on L1 line reuse between neighbouring warps;
+    // at 4 CTAs or with padded rings it measured 2.95 vs 2.05 ms at 8192^2.)
     return sizeof(double2) * 3 * npairs<MODE>() * BX + (TMA ? sizeof(double) * RSLOTS * nraw<MODE>() * RW : 0);
 }
 
