@@ -57,11 +57,8 @@ def ghost_rows(field: np.ndarray, rank: int, nranks: int, periodic_y: bool, exch
 def slab_fields(nx: int, ny: int, t: float, rank: int, nranks: int):
     """The benchmark workload restricted to this rank's rows."""
     from .workloads import mms_fields
-    g, q, b = mms_fields(nx, ny, t)
     j0, j1 = partition(ny, nranks)[rank]
-    q = q.reshape(5, ny, nx)[:, j0:j1].reshape(-1).copy()
-    b = b.reshape(ny, nx)[j0:j1].reshape(-1).copy()
-    return g, q, b
+    return mms_fields(nx, ny, t, rows=(j0, j1))  # only this rank's rows are sampled
 
 
 class SlabGroup:

@@ -14,20 +14,26 @@ from .api import BoundaryKind, make_grid
 
 
 def mms_fields(nx: int, ny: int, t: float, x_min=-1.0, x_max=1.0, y_min=-1.0, y_max=1.0,
-               kind_x=BoundaryKind.periodic, kind_y=BoundaryKind.periodic):
-    """(grid, q (5*ny*nx), b (ny*nx)) of the manufactured solution at time t."""
+               kind_x=BoundaryKind.periodic, kind_y=BoundaryKind.periodic, rows=None):
+    """(grid, q (5*ny*nx), b (ny*nx)) of the manufactured solution at time t.
+    rows=(j0, j1) samples only those global rows (a slab), q/b then hold
+    j1-j0 rows."""
     g = make_grid(x_min, x_max, y_min, y_max, nx, ny, kind_x, kind_y)
     x = g.x(np.arange(nx))
-    y = g.y(np.arange(ny))
+    if rows is not None:
+        y = g.y(np.arange(rows[0], rows[1]))
+        ny = rows[1] - rows[0]
+    else:
+        y = g.y(np.arange(ny))
     tp, fp = 2 * np.pi, 4 * np.pi
     s1x, c1x, s2x, c2x = np.sin(tp * x), np.cos(tp * x), np.sin(fp * x), np.cos(fp * x)
     s1y, c1y, s2y, c2y = np.sin(tp * y), np.cos(tp * y), np.sin(fp * y), np.cos(fp * y)
     st, ct = np.sin(tp * t), np.cos(tp * t)
     q = np.empty((5, ny, nx))
     b = np.empty((ny, nx))
-    rows = max(1, (1 << 24) // nx)  # bounded temporaries for 8192^2
-    for j0 in range(0, ny, rows):
-        sl = slice(j0, min(ny, j0 + rows))
+    chunk = max(1, (1 << 24) // nx)  # bounded temporaries for 8192^2
+    for j0 in range(0, ny, chunk):
+        sl = slice(j0, min(ny, j0 + chunk))
         S1y, C1y, S2y, C2y = s1y[sl, None], c1y[sl, None], s2y[sl, None], c2y[sl, None]
         bb = (2 / 25) * c1x * C1y + (1 / 25) * c2x * C2y
         bx = -(2 / 25) * tp * s1x * C1y - (1 / 25) * fp * s2x * C2y
