@@ -139,7 +139,6 @@ struct hsgn_ctx {
     double* d_err_part = nullptr;
     int err_part_cap = 0;
     double* d_scalar = nullptr;  // [0] err sum, [1..] misc
-    unsigned long long* d_bad = nullptr;
     double* d_rows = nullptr;
     double* h_rows = nullptr;
     StepRec* h_rec = nullptr;
@@ -314,7 +313,7 @@ static hsgn_status exchange(hsgn_ctx* c, const hsgn_state* s, int nfields) {
 // ------------------------------------------------------------------ stage launch helpers
 
 static StageArgs stage_args(hsgn_ctx* c, int mode, double t) {
-    StageArgs A = c->base;
+    StageArgs A = c->base;  // (mode: for symmetry with launch(); all modes share the base args)
     (void)mode;
     A.source = c->source;
     A.t = t;
@@ -444,8 +443,8 @@ static hsgn_status enqueue_step(hsgn_ctx* c, const hsgn_state* y, const hsgn_sta
 }
 
 // RHS evaluation into out (no depth pre-check): used by the integrator.
-static hsgn_status rhs_raw(hsgn_ctx* c, double t, const hsgn_state* q, hsgn_state* out, double lambda_override,
-                           bool shallow, unsigned long long* d_bad) {
+static hsgn_status rhs_raw(hsgn_ctx* c, double t, const hsgn_state* q, hsgn_state* out, bool shallow,
+                           unsigned long long* d_bad) {
     StageArgs A = stage_args(c, MODE_RHS, t);
     if (shallow) {
         A.lambda = 0.0;
@@ -454,7 +453,6 @@ static hsgn_status rhs_raw(hsgn_ctx* c, double t, const hsgn_state* q, hsgn_stat
         A.lam_sixth = 0.0;
         A.shallow = 1;
     }
-    (void)lambda_override;
     A.y = q->base;
     A.out = out->base;
     A.bad = d_bad;
@@ -479,7 +477,7 @@ static hsgn_status rhs_checked(hsgn_ctx* c, double t, const hsgn_state* q, hsgn_
         ++c->n_evals;  // rhs.hpp:84 counts the evaluation before throwing
         return fail(c, HSGN_EDEPTH, "tendency evaluation at t = %f: %llu nodes with non-positive depth", t, hb);
     }
-    s = rhs_raw(c, t, q, out, 0.0, shallow, &c->d_rec[0].bad[1]);
+    s = rhs_raw(c, t, q, out, shallow, &c->d_rec[0].bad[1]);
     if (s) return s;
     CK(cudaStreamSynchronize(c->stream));
     return HSGN_OK;
@@ -950,7 +948,7 @@ static hsgn_status wrms(hsgn_ctx* c, const hsgn_state* x, const hsgn_state* ref,
 static hsgn_status rhs_eval(hsgn_ctx* c, double t, const hsgn_state* q, hsgn_state* out) {
     unsigned long long* d_bad = &c->d_rec[0].bad[0];
     CK(cudaMemsetAsync(d_bad, 0, sizeof(unsigned long long), c->stream));
-    hsgn_status s = rhs_raw(c, t, q, out, 0.0, false, d_bad);
+    hsgn_status s = rhs_raw(c, t, q, out, false, d_bad);
     if (s) return s;
     unsigned long long hb = 0;
     CK(cudaMemcpyAsync(&hb, d_bad, sizeof hb, cudaMemcpyDeviceToHost, c->stream));
@@ -1536,7 +1534,7 @@ hsgn_status hsgn_group_rhs(hsgn_group* G, double t, const hsgn_gstate* q, hsgn_g
         if (s) return s;
         cudaMemsetAsync(&c->d_rec[0].bad[0], 0, sizeof(unsigned long long), c->stream);
         group_wait_pulls(G, r);
-        if ((s = rhs_raw(c, t, q->p[r], out->p[r], 0.0, false, &c->d_rec[0].bad[0]))) return s;
+        if ((s = rhs_raw(c, t, q->p[r], out->p[r], false, &c->d_rec[0].bad[0]))) return s;
         cudaEventRecord(G->evk[r], c->stream);
     }
     hsgn_status s = group_pull(G, out->p, 5);

@@ -35,7 +35,10 @@
 
 namespace hsgn_dev {
 
-constexpr int BX = 128;     // threads per CTA == columns touched per tile
+#ifndef HSGN_BX
+#define HSGN_BX 128
+#endif
+constexpr int BX = HSGN_BX;  // threads per CTA == columns touched per tile
 constexpr int WX = BX - 2;  // finished columns per tile
 #ifndef HSGN_MIN_BLOCKS
 #define HSGN_MIN_BLOCKS 0  // 0: per-stage choice in min_blocks()
@@ -47,7 +50,8 @@ template <int MODE>
 __host__ __device__ constexpr int min_blocks() {
     // measured (r1): S2 (largest ring, 16 raw inputs) is best at 3 CTAs/SM;
     // the other stages fit 96 registers without spills and run best at 5
-    return HSGN_MIN_BLOCKS > 0 ? HSGN_MIN_BLOCKS : (MODE == MODE_S2 ? 3 : 5);
+    // (expressed as resident warps per SM: 12 for S2, 20 for the others)
+    return HSGN_MIN_BLOCKS > 0 ? HSGN_MIN_BLOCKS : (MODE == MODE_S2 ? 12 : 20) / (BX / 32);
 }
 
 // Per-field device pointers (kernel parameters live in the constant bank, so
@@ -334,6 +338,9 @@ struct Thr {
 };
 
 // Distance (rows) of the bulk L2 prefetch ahead of the register loads.
+#ifndef HSGN_EARLY_PF  // stages with <= 6 raw inputs issue the next-row loads before products
+#define HSGN_EARLY_PF 0
+#endif
 #ifndef HSGN_L2_PF
 #define HSGN_L2_PF 0
 #endif
@@ -407,7 +414,7 @@ __device__ __forceinline__ void march_row(const StageArgs& A, const KPtrs& P, Th
     // needs two raw register sets and a 6x-unrolled march: measured slower in
     // round 1 -- spills in S1/S2, I-cache in S3 -- so EARLY stays off; raw and
     // raw_next may then alias.)
-    constexpr bool EARLY = false;
+    constexpr bool EARLY = HSGN_EARLY_PF && nraw<MODE>() <= 6;
     if (!TMA && EARLY && jn < T.j1) load_raw<MODE>(P, (unsigned)map_row(A, jn + 1) * nx + T.col, raw_next);
     if (!TMA && HSGN_L2_PF > 1 && jn + HSGN_L2_PF <= T.j1) l2_prefetch_row<MODE>(A, T, jn + HSGN_L2_PF);
     if (TMA) {  // raw row jn lives in raw slot (SC+2)%3; row j+3 goes into slot (SC+1)%3
@@ -421,7 +428,8 @@ __device__ __forceinline__ void march_row(const StageArgs& A, const KPtrs& P, Th
         const bool ok = products<MODE>(A, raw, ring + SN * (NP * BX) + T.tid, yn);
         if (T.finish && jn < T.j1 && !ok) ++T.bad;
     }
-    if (!TMA && !EARLY && jn < T.j1) load_raw<MODE>(P, (unsigned)map_row(A, jn + 1) * nx + T.col, raw_next);
+    if (!TMA && !EARLY && jn < T.j1) load_raw<MODE>(P, (unsigned)map_row(A, jn + 1) * nx + T.col, raw);
+    if (!TMA && EARLY) raw = raw_next;  // (register moves: the 3x unroll cannot alternate two sets)
     // One barrier per row: row j's ring entries (written one step ago) become
     // visible, and this step's writes to slot SN are ordered after the last
     // reads of that slot (finish of row j-2, before the previous barrier).
@@ -667,12 +675,13 @@ __global__ void __launch_bounds__(BX, min_blocks<MODE>()) sgn_stage_kernel(const
 
     // ---- march, unrolled by 3: row j lives in ring slot (j-j0)%3 and register
     // set {a,b,c}[(j-j0)%3]; step SC reads set SC+2 (row j-1), writes SC+1.
+    Raw raw2;  // next-row prefetch target when it overlaps products (EARLY)
     for (int j = j0; j < T.j1; j += 3) {
-        march_row<MODE, KIND, TMA, 0>(A, P, T, ring, rawring, bars, j0, j, yc, yb, raw, raw);
+        march_row<MODE, KIND, TMA, 0>(A, P, T, ring, rawring, bars, j0, j, yc, yb, raw, raw2);
         if (j + 1 >= T.j1) break;
-        march_row<MODE, KIND, TMA, 1>(A, P, T, ring, rawring, bars, j0, j + 1, ya, yc, raw, raw);
+        march_row<MODE, KIND, TMA, 1>(A, P, T, ring, rawring, bars, j0, j + 1, ya, yc, raw, raw2);
         if (j + 2 >= T.j1) break;
-        march_row<MODE, KIND, TMA, 2>(A, P, T, ring, rawring, bars, j0, j + 2, yb, ya, raw, raw);
+        march_row<MODE, KIND, TMA, 2>(A, P, T, ring, rawring, bars, j0, j + 2, yb, ya, raw, raw2);
     }
 
     // ---- block reductions (fixed order inside the block)
