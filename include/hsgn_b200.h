@@ -160,6 +160,38 @@ hsgn_status hsgn_solve(hsgn_ctx* ctx, const hsgn_state* q0, double t0, double t_
                        const hsgn_cfg* cfg, hsgn_state* q_out, hsgn_record* rec, hsgn_observer obs,
                        void* user);
 
+/* ------------------------------------------------------------ run recorder */
+
+/* RunRecorder (io.hpp:107-219) on the device: gauge samples h + b at the
+ * nearest nodes of gauge_xy (n_gauges (x, y) pairs, io.hpp:38-48) after
+ * every accepted step, the conservation row (t, total mass, total energy,
+ * semidiscrete energy rate) every conservation_stride accepted steps
+ * (counting the initial state), and snapshots of the accepted state closest
+ * to each target time.  Fixed-step runs keep their CUDA-graph chunks (the
+ * gauge gather is captured in them).  Whole-grid contexts only. */
+typedef struct hsgn_recorder hsgn_recorder;
+hsgn_status hsgn_recorder_create(hsgn_ctx* ctx, int32_t n_gauges, const double* gauge_xy, int32_t n_targets,
+                                 const double* targets, int64_t conservation_stride, hsgn_recorder** out);
+hsgn_status hsgn_recorder_destroy(hsgn_recorder* r);
+/* adaptive_solve with the recorder attached as its AcceptObserver
+ * (cli.hpp:100-111); obs may be NULL. */
+hsgn_status hsgn_solve_recorded(hsgn_ctx* ctx, const hsgn_state* q0, double t0, double t_final,
+                                const hsgn_cfg* cfg, hsgn_state* q_out, hsgn_record* rec, hsgn_observer obs,
+                                void* user, hsgn_recorder* r);
+hsgn_status hsgn_recorder_counts(const hsgn_recorder* r, int64_t* gauge_rows, int64_t* cons_rows,
+                                 int32_t* snapshots);
+/* node (i, j) and coordinates of gauge k */
+hsgn_status hsgn_recorder_gauge_node(const hsgn_recorder* r, int32_t k, int32_t* i, int32_t* j, double* x,
+                                     double* y);
+/* t[rows], values[rows * n_gauges] */
+hsgn_status hsgn_recorder_gauges(const hsgn_recorder* r, double* t, double* values);
+/* rows4[rows * 4] = (t, mass, energy, energy_rate) */
+hsgn_status hsgn_recorder_conservation(const hsgn_recorder* r, double* rows4);
+/* snapshot k: target time, time of the state used, and the state (host
+ * layout, may be NULL) */
+hsgn_status hsgn_recorder_snapshot(const hsgn_recorder* r, int32_t k, double* target, double* actual,
+                                   double* host_state);
+
 /* The bare fused fixed-step pipeline used by the benchmark: `steps` BS3 steps
  * of size dt on (y, k1) in place (k1 must hold f(y) on entry; it holds f(y)
  * of the new state on return, FSAL).  Graph-captured.  Returns HSGN_EDEPTH

@@ -11,6 +11,7 @@
 // prebuilt file.  Never linked by the product library.
 
 #include <hsgn/analysis.hpp>
+#include <hsgn/io.hpp>
 #include <hsgn/manufactured_generated.hpp>
 #include <hsgn/model.hpp>
 #include <hsgn/rhs.hpp>
@@ -190,6 +191,38 @@ int ref_solve(const orc_grid* g, const orc_phys* phys, const double* b, int sour
     std::snprintf(rec_out->reason, sizeof rec_out->reason, "%s", rec.abort_reason.c_str());
     if (hist_n)
         *hist_n = nh;
+    return rec.aborted ? 1 : 0;
+}
+
+// cmd_run's recorder wiring (cli.hpp:100-116): adaptive_solve with
+// RunRecorder::on_accept as the observer, then flush() -- the reference
+// writes gauges.csv, conservation.csv and snapshot_t*.csv into out_dir.
+int ref_run_recorded(const orc_grid* g, const orc_phys* phys, const double* b, int source_kind,
+                     const double* q0, double t0, double t_final, const orc_cfg* c, double* q_out,
+                     orc_record* rec_out, const char* out_dir, int n_gauges, const double* gauge_xy,
+                     int n_targets, const double* targets, int64_t stride) {
+    Grid2D grid = grid_of(g);
+    RhsContext ctx = context_of(grid, phys, b, source_kind);
+    StateField qs(grid);
+    to_state(q0, qs);
+    std::vector<std::array<double, 2>> gauges;
+    for (int k = 0; k < n_gauges; ++k) gauges.push_back({gauge_xy[2 * k], gauge_xy[2 * k + 1]});
+    std::vector<double> tg(targets, targets + n_targets);
+    std::filesystem::create_directories(out_dir);  // as cmd_run does (cli.hpp:93)
+    RunRecorder recorder(ctx, out_dir, gauges, tg, stride);  // io.hpp:109-118
+    SolutionRecord rec = adaptive_solve(
+        [&ctx](double t, const StateField& q, StateField& out) { rhs(ctx, t, q, out); }, qs, t0,
+        t_final, cfg_of(c),
+        [&recorder](double t, const StateField& q, const StateField& qt) { recorder.on_accept(t, q, qt); });
+    recorder.flush();  // io.hpp:155-185
+    from_state(rec.q, q_out);
+    rec_out->t = rec.t;
+    rec_out->accepted = rec.accepted;
+    rec_out->rejected = rec.rejected;
+    rec_out->rhs_evals = rec.rhs_evals;
+    rec_out->rhs_evals_setup = rec.rhs_evals_setup;
+    rec_out->aborted = rec.aborted ? 1 : 0;
+    std::snprintf(rec_out->reason, sizeof rec_out->reason, "%s", rec.abort_reason.c_str());
     return rec.aborted ? 1 : 0;
 }
 

@@ -9,11 +9,12 @@ from .api import (AcceptObserver, BoundaryKind, DepthError, DeviceState, Grid2D,
                   bs3_fixed_steps, direction_spacing, discrete_l2_error, energy_rate, eoc, init_auxiliary,
                   make_grid, make_rhs_context, mass_weighted_sum, rhs, rhs_periodic, rhs_reflecting, rhs_shallow_water,
                   total_energy, total_mass)
+from .recorder import RunRecorder
 
 __all__ = [
     "AcceptObserver", "BoundaryKind", "DepthError", "DeviceState", "Grid2D", "HsgnError", "IntegratorConfig",
     "PhysSetup", "RhsContext", "SolutionRecord", "StateField", "adaptive_solve", "bs3_fixed_steps",
     "direction_spacing", "discrete_l2_error", "energy_rate", "eoc", "init_auxiliary", "make_grid",
     "make_rhs_context", "mass_weighted_sum", "rhs", "rhs_periodic", "rhs_reflecting", "rhs_shallow_water", "total_energy",
-    "total_mass",
+    "total_mass", "RunRecorder",
 ]

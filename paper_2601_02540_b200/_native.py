@@ -113,6 +113,15 @@ def lib() -> C.CDLL:
     f("hsgn_group_rhs", C.c_int, GRP, D, GST, GST, C.POINTER(I64))
     f("hsgn_group_bs3_fixed_steps", C.c_int, GRP, GST, GST, D, D, I64, C.POINTER(I64))
     f("hsgn_group_reduce", C.c_int, GRP, I32, GST, GST, PD)
+    REC = C.c_void_p
+    f("hsgn_recorder_create", C.c_int, CTX, I32, PD, I32, PD, I64, C.POINTER(REC))
+    f("hsgn_recorder_destroy", C.c_int, REC)
+    f("hsgn_solve_recorded", C.c_int, CTX, STATE, D, D, CF, STATE, RC, OBSERVER, C.c_void_p, REC)
+    f("hsgn_recorder_counts", C.c_int, REC, C.POINTER(I64), C.POINTER(I64), C.POINTER(I32))
+    f("hsgn_recorder_gauge_node", C.c_int, REC, I32, C.POINTER(I32), C.POINTER(I32), PD, PD)
+    f("hsgn_recorder_gauges", C.c_int, REC, PD, PD)
+    f("hsgn_recorder_conservation", C.c_int, REC, PD)
+    f("hsgn_recorder_snapshot", C.c_int, REC, I32, PD, PD, PD)
     _lib = L
     return L
 
@@ -130,4 +139,6 @@ EXPORTS = [
     "hsgn_group_create", "hsgn_group_destroy", "hsgn_group_last_error", "hsgn_group_state_alloc",
     "hsgn_group_state_free", "hsgn_group_state_upload", "hsgn_group_state_download", "hsgn_group_rhs",
     "hsgn_group_bs3_fixed_steps", "hsgn_group_reduce",
+    "hsgn_recorder_create", "hsgn_recorder_destroy", "hsgn_solve_recorded", "hsgn_recorder_counts",
+    "hsgn_recorder_gauge_node", "hsgn_recorder_gauges", "hsgn_recorder_conservation", "hsgn_recorder_snapshot",
 ]

@@ -235,6 +235,11 @@ class RhsContext:
             raise HsgnError(f"hsgn_ctx_create failed: {N.STATUS_NAMES.get(st, st)} (is a B200 visible?)")
         self.ny_local = self.j_end - self.j_begin
         self._source = None
+        self._b = b
+
+    def bathymetry(self) -> np.ndarray:
+        """ctx.phys.b of this context's rows (host copy)."""
+        return self._b
 
     # ctx.source (rhs.hpp:24-26): None or "manufactured"
     @property
@@ -427,12 +432,13 @@ AcceptObserver = Callable[[float, DeviceState, DeviceState], None]
 
 
 def adaptive_solve(ctx: RhsContext, q0, t0: float, t_final: float, cfg: IntegratorConfig = None,
-                   on_accept: Optional[AcceptObserver] = None, out: Optional[DeviceState] = None
-                   ) -> SolutionRecord:
+                   on_accept: Optional[AcceptObserver] = None, out: Optional[DeviceState] = None,
+                   recorder=None) -> SolutionRecord:
     """time_integration.hpp:209-350 on the fused device pipeline.  The RHS is
     the context's own split form (the generic callable of the reference
     cannot be fused into stage kernels).  on_accept receives device states
-    valid only during the call."""
+    valid only during the call; ``recorder`` (a recorder.RunRecorder) is the
+    on-device AcceptObserver of cli.hpp:100-111."""
     cfg = cfg or IntegratorConfig()
     dq0, _ = _as_device(ctx, q0)
     dout = out if out is not None else DeviceState(ctx)
@@ -447,11 +453,13 @@ def adaptive_solve(ctx: RhsContext, q0, t0: float, t_final: float, cfg: Integrat
             err_box.append(e)
 
     cb = N.OBSERVER(_obs) if on_accept is not None else N.OBSERVER()
-    st = N.lib().hsgn_solve(ctx._h, dq0._h, float(t0), float(t_final), C.byref(cfgc), dout._h, C.byref(rec),
-                            cb, None)
+    st = N.lib().hsgn_solve_recorded(ctx._h, dq0._h, float(t0), float(t_final), C.byref(cfgc), dout._h,
+                                     C.byref(rec), cb, None, recorder._h if recorder is not None else None)
     if err_box:
         raise err_box[0]
     _check(ctx, st, "adaptive_solve")
+    if recorder is not None:
+        recorder.write_snapshots()
     res = SolutionRecord(None, rec.t, rec.accepted, rec.rejected, rec.rhs_evals, rec.rhs_evals_setup,
                          bool(rec.aborted), rec.reason.decode())
     res.q = dout.download() if out is None else None

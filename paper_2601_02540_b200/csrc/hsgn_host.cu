@@ -30,7 +30,9 @@ cudaError_t launch_stage(int mode, const StageArgs& A, cudaStream_t st);
 int stage_grid_blocks(const StageArgs& A);
 cudaError_t launch_sum_partials(const double* part, int n, double* out, cudaStream_t st);
 // sgn_aux.cu
-
+cudaError_t launch_cons_rows(const AuxArgs& A, const double* q, const double* qt, double* rows, cudaStream_t st);
+cudaError_t launch_gauges(const double* h, const double* b, const long long* idx, int n, double* out,
+                          cudaStream_t st);
 cudaError_t launch_row_sums(const AuxArgs& A, int kind, const double* q, const double* qt, int field,
                             double* rows, cudaStream_t st);
 cudaError_t launch_depth_check(const double* h, long long n, unsigned long long* bad, cudaStream_t st);
@@ -142,12 +144,41 @@ struct hsgn_ctx {
     double* d_rows = nullptr;
     double* h_rows = nullptr;
     StepRec* h_rec = nullptr;
-    std::map<std::tuple<int, int, double, uint64_t, uint64_t>, FixedGraph> graphs;
+    std::map<std::tuple<int, int, uint64_t, uint64_t, uint64_t>, FixedGraph> graphs;  // (steps, parity, gauges, dt, rpb)
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     double last_ms = 0.0;
     int64_t last_kernels = 0;
     // NCCL
     nccl_comm comm = nullptr;
+};
+
+// On-device run recorder (io.hpp:107-219 RunRecorder): gauge samples are
+// gathered by a kernel into a staging block (captured per step in the
+// fixed-step graphs), conservation rows are one fused row-sum pass at the
+// stride, snapshots are stream-ordered D2H copies into pinned memory.
+struct hsgn_recorder {
+    hsgn_ctx* c = nullptr;
+    std::vector<int32_t> gi, gj;
+    std::vector<double> gx, gy;
+    long long* d_idx = nullptr;  // j*nx + i per gauge
+    double* d_gauge = nullptr;   // staging: gauge_cap rows x n_gauges
+    double* h_gauge = nullptr;   // pinned mirror
+    int gauge_cap = 0;
+    double* d_cons = nullptr;  // 3 x ny row sums (mass, energy, energy rate)
+    double* h_cons = nullptr;
+    std::vector<double> targets;  // sorted
+    size_t next_target = 0;
+    int64_t stride = 1;
+    bool first = true;
+    double prev_t = 0.0;
+    int64_t accept_count = 0;
+    // results
+    std::vector<double> gauge_t, gauge_vals, cons;  // cons: (t, mass, energy, rate) rows
+    struct Snap {
+        double target, actual;
+        double* host;  // pinned, 5 * nx * ny
+    };
+    std::vector<Snap> snaps;
 };
 
 namespace {
@@ -840,9 +871,14 @@ uint64_t bits_of(double v) {
     return u;
 }
 
-// Capture (or fetch) a graph of `steps` fused steps starting at buffer parity p.
-hsgn_status get_fixed_graph(hsgn_ctx* c, int steps, int parity, double dt, FixedGraph** out) {
-    auto key = std::make_tuple(steps, parity, 0.0, bits_of(dt), (uint64_t)c->base.rows_per_block);
+// Capture (or fetch) a graph of `steps` fused steps starting at buffer parity
+// p; with a recorder that has gauges, each step also samples them (row s of
+// the staging block).
+hsgn_status get_fixed_graph(hsgn_ctx* c, int steps, int parity, double dt, const hsgn_recorder* R,
+                            FixedGraph** out) {
+    const bool gauges = R && !R->gi.empty();
+    auto key = std::make_tuple(steps, parity, gauges ? (uint64_t)(uintptr_t)R->d_gauge : 0ull, bits_of(dt),
+                               (uint64_t)c->base.rows_per_block);
     auto it = c->graphs.find(key);
     if (it != c->graphs.end()) {
         *out = &it->second;
@@ -858,6 +894,11 @@ hsgn_status get_fixed_graph(hsgn_ctx* c, int steps, int parity, double dt, Fixed
         const int p = (parity + s) & 1;
         st = enqueue_step(c, Y[p], K[p], &c->ws[4], Y[p ^ 1], K[p ^ 1], nullptr, &c->d_rec[s],
                           s ? &c->d_rec[s - 1] : nullptr, 0.0, dt, false, 0, 0, nullptr);
+        if (!st && gauges) {
+            cudaError_t ge = launch_gauges(Y[p ^ 1]->base, c->b, R->d_idx, (int)R->gi.size(),
+                                           R->d_gauge + (size_t)s * R->gi.size(), c->stream);
+            if (ge != cudaSuccess) st = fail(c, HSGN_ECUDA, "gauge launch: %s", cudaGetErrorString(ge));
+        }
     }
     cudaError_t e = cudaStreamEndCapture(c->stream, &g);
     if (st) {
@@ -882,14 +923,16 @@ hsgn_status get_fixed_graph(hsgn_ctx* c, int steps, int parity, double dt, Fixed
 // Returns the number of completed steps and the failure kind (0 none,
 // 1 depth at stage k (fail_stage), 2 floor).
 static hsgn_status run_fixed_chunk(hsgn_ctx* c, int parity, int steps, double t, double dt, int* done,
-                                   int* fail_kind, int* fail_stage, int64_t* kernels) {
+                                   int* fail_kind, int* fail_stage, int64_t* kernels,
+                                   const hsgn_recorder* R = nullptr) {
+    const bool gauges = R && !R->gi.empty();
     hsgn_status st;
     if ((st = ensure_ws(c, steps))) return st;
     if (c->source == 0 && c->nranks == 1) {
         FixedGraph* fg = nullptr;
-        if ((st = get_fixed_graph(c, steps, parity, dt, &fg))) return st;
+        if ((st = get_fixed_graph(c, steps, parity, dt, R, &fg))) return st;
         CK(cudaGraphLaunch(fg->exec, c->stream));
-        if (kernels) *kernels += 3 * steps;
+        if (kernels) *kernels += (gauges ? 4 : 3) * steps;
     } else {
         hsgn_state* Y[2] = {&c->ws[0], &c->ws[1]};
         hsgn_state* K[2] = {&c->ws[2], &c->ws[3]};
@@ -900,6 +943,11 @@ static hsgn_status run_fixed_chunk(hsgn_ctx* c, int parity, int steps, double t,
             st = enqueue_step(c, Y[p], K[p], &c->ws[4], Y[p ^ 1], K[p ^ 1], nullptr, &c->d_rec[s],
                               s ? &c->d_rec[s - 1] : nullptr, ts, dt, false, 0, 0, kernels);
             if (st) return st;
+            if (gauges) {
+                CK(launch_gauges(Y[p ^ 1]->base, c->b, R->d_idx, (int)R->gi.size(),
+                                 R->d_gauge + (size_t)s * R->gi.size(), c->stream));
+                if (kernels) ++*kernels;
+            }
             ts = ts + dt;
         }
     }
@@ -957,9 +1005,85 @@ static hsgn_status rhs_eval(hsgn_ctx* c, double t, const hsgn_state* q, hsgn_sta
     return HSGN_OK;
 }
 
+// ------------------------------------------------------------------ recorder
+
+// Append `rows` staged gauge rows (sample times ts[0..rows)) to the series.
+static hsgn_status rec_collect_gauges(hsgn_recorder* R, const double* ts, int rows) {
+    hsgn_ctx* c = R->c;
+    const size_t ng = R->gi.size();
+    if (!ng || rows <= 0) return HSGN_OK;
+    CK(cudaMemcpyAsync(R->h_gauge, R->d_gauge, sizeof(double) * ng * rows, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    for (int s = 0; s < rows; ++s) {
+        R->gauge_t.push_back(ts[s]);
+        R->gauge_vals.insert(R->gauge_vals.end(), R->h_gauge + s * ng, R->h_gauge + (s + 1) * ng);
+    }
+    return HSGN_OK;
+}
+
+// Sample the gauges of q at time t (one row, staged then collected).
+static hsgn_status rec_gauges_now(hsgn_recorder* R, double t, const hsgn_state* q) {
+    hsgn_ctx* c = R->c;
+    if (R->gi.empty()) return HSGN_OK;
+    CK(launch_gauges(q->base, c->b, R->d_idx, (int)R->gi.size(), R->d_gauge, c->stream));
+    return rec_collect_gauges(R, &t, 1);
+}
+
+// take_snapshot (io.hpp:197-204): stream-ordered copy into pinned memory; the
+// host does not wait (the CSV is written by the caller from the copy).
+static hsgn_status rec_snapshot(hsgn_recorder* R, double target, double actual, const hsgn_state* q) {
+    hsgn_ctx* c = R->c;
+    const size_t n = (size_t)c->grid.nx * c->ny_loc;
+    hsgn_recorder::Snap sn{target, actual, nullptr};
+    CK(cudaMallocHost(&sn.host, sizeof(double) * 5 * n));
+    R->snaps.push_back(sn);
+    for (int f = 0; f < 5; ++f)
+        CK(cudaMemcpyAsync(sn.host + f * n, q->f(f), sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+    return HSGN_OK;
+}
+
+// RunRecorder::on_accept (io.hpp:120-152) for the state q (tendency qt) at
+// time t; prev is the previously accepted state (the other buffer of the
+// integrator's pair).  The gauge row is sampled by the caller.
+static hsgn_status rec_accept(hsgn_recorder* R, double t, const hsgn_state* q, const hsgn_state* qt,
+                              const hsgn_state* prev) {
+    hsgn_ctx* c = R->c;
+    hsgn_status st;
+    if (R->first) {
+        R->first = false;
+        R->prev_t = t;
+        while (R->next_target < R->targets.size() && R->targets[R->next_target] <= t)
+            if ((st = rec_snapshot(R, R->targets[R->next_target++], t, q))) return st;
+    } else {
+        while (R->next_target < R->targets.size() && R->targets[R->next_target] <= t) {
+            const double target = R->targets[R->next_target++];
+            const bool prev_closer = target - R->prev_t < t - target;
+            if ((st = rec_snapshot(R, target, prev_closer ? R->prev_t : t, prev_closer ? prev : q))) return st;
+        }
+        R->prev_t = t;
+    }
+    if (R->accept_count % R->stride == 0) {
+        const int ny = c->ny_loc;
+        CK(launch_cons_rows(c->aux, q->base, qt->base, R->d_cons, c->stream));
+        CK(cudaMemcpyAsync(R->h_cons, R->d_cons, sizeof(double) * 3 * ny, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        R->cons.push_back(t);
+        for (int k = 0; k < 3; ++k) R->cons.push_back(outer_sum(&c->grid, R->h_cons + (size_t)k * ny, 0, ny));
+    }
+    ++R->accept_count;
+    return HSGN_OK;
+}
+
 extern "C" hsgn_status hsgn_solve(hsgn_ctx* c, const hsgn_state* q0, double t0, double t_final, const hsgn_cfg* cfg,
                                   hsgn_state* q_out, hsgn_record* rec, hsgn_observer obs, void* user) {
+    return hsgn_solve_recorded(c, q0, t0, t_final, cfg, q_out, rec, obs, user, nullptr);
+}
+
+extern "C" hsgn_status hsgn_solve_recorded(hsgn_ctx* c, const hsgn_state* q0, double t0, double t_final,
+                                           const hsgn_cfg* cfg, hsgn_state* q_out, hsgn_record* rec,
+                                           hsgn_observer obs, void* user, hsgn_recorder* R) {
     if (!c || !q0 || !cfg || !q_out || !rec) return HSGN_EINVAL;
+    if (R && R->c != c) return fail(c, HSGN_EINVAL, "recorder belongs to another context");
     CK(cudaSetDevice(c->device));
     std::memset(rec, 0, sizeof *rec);
     rec->t = t0;
@@ -1047,6 +1171,10 @@ extern "C" hsgn_status hsgn_solve(hsgn_ctx* c, const hsgn_state* q0, double t0, 
         }
         rec->rhs_evals += rec->rhs_evals_setup;
     }
+    if (R) {
+        if ((st = rec_gauges_now(R, t, &c->ws[0]))) return st;
+        if ((st = rec_accept(R, t, &c->ws[0], &c->ws[2], nullptr))) return st;
+    }
     if (obs) {
         CK(cudaStreamSynchronize(c->stream));
         obs(t, &c->ws[0], &c->ws[2], user);
@@ -1069,19 +1197,29 @@ extern "C" hsgn_status hsgn_solve(hsgn_ctx* c, const hsgn_state* q0, double t0, 
             return abort_with(why);
         }
         if (fixed && !obs && !clipped) {
-            // plan a chunk of unclipped steps: replicate the host t sequence exactly
+            // plan a chunk of unclipped steps: replicate the host t sequence exactly.
+            // With a recorder the chunk ends at the next conservation record or
+            // at the step that crosses the next snapshot target, so recorder
+            // work inside a chunk is only the (graph-captured) gauge sample.
+            int cap = CHUNK;
+            if (R) {
+                const int64_t k = R->accept_count, krec = (k + R->stride - 1) / R->stride * R->stride;
+                cap = (int)std::min<int64_t>(cap, krec - k + 1);
+            }
             int n = 0;
             double tt = t;
-            while (n < CHUNK && rec->accepted + rec->rejected + n < cfg->max_steps &&
+            double ts[CHUNK];
+            while (n < cap && rec->accepted + rec->rejected + n < cfg->max_steps &&
                    tt < t_final - tiny * smax(1.0, std::fabs(t_final)) && !(dt >= t_final - tt) &&
                    (dt > tiny * smax(1.0, std::fabs(tt)))) {
                 tt = tt + dt;
-                ++n;
+                ts[n++] = tt;
+                if (R && R->next_target < R->targets.size() && R->targets[R->next_target] <= tt) break;
             }
             if (n >= 2) {
-                if (n & 1) --n;  // even chunks keep the buffer parity
+                if ((n & 1) && !R) --n;  // even chunks keep the buffer parity (fewer graphs)
                 int done = 0, fk = 0, fs_ = 0;
-                if ((st = run_fixed_chunk(c, p, n, t, dt, &done, &fk, &fs_, &kernels))) return st;
+                if ((st = run_fixed_chunk(c, p, n, t, dt, &done, &fk, &fs_, &kernels, R))) return st;
                 for (int s = 0; s < done; ++s) {
                     t = t + dt;
                     ++rec->accepted;
@@ -1089,6 +1227,16 @@ extern "C" hsgn_status hsgn_solve(hsgn_ctx* c, const hsgn_state* q0, double t0, 
                     p ^= 1;
                 }
                 c->n_evals += 3 * (int64_t)done;
+                if (R) {
+                    if ((st = rec_collect_gauges(R, ts, done))) return st;
+                    if (done == n) {  // steps 1..n-1 carry no record by construction
+                        R->accept_count += n - 1;
+                        R->prev_t = ts[n - 2];
+                        if ((st = rec_accept(R, t, &c->ws[p], &c->ws[2 + p], &c->ws[p ^ 1]))) return st;
+                    } else {
+                        R->accept_count += done;
+                    }
+                }
                 if (fk) {
                     if (fk == 1) {
                         rec->rhs_evals += fs_;
@@ -1158,6 +1306,10 @@ extern "C" hsgn_status hsgn_solve(hsgn_ctx* c, const hsgn_state* q0, double t0, 
                 dt = smin(dt * fac, cfg->dt_max);
                 err_prev = smax(err, 1e-10);
             }
+            if (R) {
+                if ((st = rec_gauges_now(R, t, &c->ws[p]))) return st;
+                if ((st = rec_accept(R, t, &c->ws[p], &c->ws[2 + p], &c->ws[p ^ 1]))) return st;
+            }
             if (obs) obs(t, &c->ws[p], &c->ws[2 + p], user);
         } else {
             ++rec->rejected;
@@ -1169,6 +1321,113 @@ extern "C" hsgn_status hsgn_solve(hsgn_ctx* c, const hsgn_state* q0, double t0, 
     CK(cudaStreamSynchronize(c->stream));
     rec->t = t;
     c->last_kernels = kernels;
+    return HSGN_OK;
+}
+
+extern "C" hsgn_status hsgn_recorder_create(hsgn_ctx* c, int32_t n_gauges, const double* gauge_xy,
+                                            int32_t n_targets, const double* targets, int64_t conservation_stride,
+                                            hsgn_recorder** out) {
+    if (!c || !out || n_gauges < 0 || n_targets < 0 || (n_gauges && !gauge_xy) || (n_targets && !targets))
+        return HSGN_EINVAL;
+    *out = nullptr;
+    if (conservation_stride < 1)  // config.hpp:234-237
+        return fail(c, HSGN_EINVAL, "conservation_stride must be >= 1");
+    if (c->nranks != 1) return fail(c, HSGN_EINVAL, "the recorder needs a whole-grid context");
+    CK(cudaSetDevice(c->device));
+    hsgn_recorder* R = new hsgn_recorder;
+    R->c = c;
+    R->stride = conservation_stride;
+    const hsgn_grid& g = c->grid;
+    std::vector<long long> idx;
+    for (int k = 0; k < n_gauges; ++k) {  // nearest_node (io.hpp:38-48)
+        const double x = gauge_xy[2 * k], y = gauge_xy[2 * k + 1];
+        const int i = std::clamp(static_cast<int>(std::lround((x - g.x_min) / c->dx)), 0, g.nx - 1);
+        const int j = std::clamp(static_cast<int>(std::lround((y - g.y_min) / c->dy)), 0, g.ny - 1);
+        R->gi.push_back(i);
+        R->gj.push_back(j);
+        R->gx.push_back(g.x_min + i * c->dx);  // Grid2D::x / y (grid.hpp:24-25)
+        R->gy.push_back(g.y_min + j * c->dy);
+        idx.push_back((long long)j * g.nx + i);
+    }
+    R->targets.assign(targets, targets + n_targets);
+    std::sort(R->targets.begin(), R->targets.end());
+    auto cleanup_fail = [&](cudaError_t e) {
+        hsgn_recorder_destroy(R);
+        return fail(c, HSGN_ECUDA, "recorder allocation: %s", cudaGetErrorString(e));
+    };
+    cudaError_t e;
+    R->gauge_cap = 64;  // >= the fixed-step chunk
+    if (n_gauges) {
+        if ((e = cudaMalloc(&R->d_idx, sizeof(long long) * n_gauges))) return cleanup_fail(e);
+        if ((e = cudaMemcpy(R->d_idx, idx.data(), sizeof(long long) * n_gauges, cudaMemcpyHostToDevice)))
+            return cleanup_fail(e);
+        if ((e = cudaMalloc(&R->d_gauge, sizeof(double) * n_gauges * R->gauge_cap))) return cleanup_fail(e);
+        if ((e = cudaMallocHost(&R->h_gauge, sizeof(double) * n_gauges * R->gauge_cap))) return cleanup_fail(e);
+    }
+    if ((e = cudaMalloc(&R->d_cons, sizeof(double) * 3 * c->ny_loc))) return cleanup_fail(e);
+    if ((e = cudaMallocHost(&R->h_cons, sizeof(double) * 3 * c->ny_loc))) return cleanup_fail(e);
+    *out = R;
+    return HSGN_OK;
+}
+
+extern "C" hsgn_status hsgn_recorder_destroy(hsgn_recorder* R) {
+    if (!R) return HSGN_OK;
+    if (R->c) cudaSetDevice(R->c->device);
+    if (R->c) cudaStreamSynchronize(R->c->stream);  // pending snapshot copies
+    cudaFree(R->d_idx);
+    cudaFree(R->d_gauge);
+    cudaFreeHost(R->h_gauge);
+    cudaFree(R->d_cons);
+    cudaFreeHost(R->h_cons);
+    for (auto& s : R->snaps) cudaFreeHost(s.host);
+    delete R;
+    return HSGN_OK;
+}
+
+extern "C" hsgn_status hsgn_recorder_counts(const hsgn_recorder* R, int64_t* gauge_rows, int64_t* cons_rows,
+                                            int32_t* snapshots) {
+    if (!R) return HSGN_EINVAL;
+    if (gauge_rows) *gauge_rows = (int64_t)R->gauge_t.size();
+    if (cons_rows) *cons_rows = (int64_t)(R->cons.size() / 4);
+    if (snapshots) *snapshots = (int32_t)R->snaps.size();
+    return HSGN_OK;
+}
+
+extern "C" hsgn_status hsgn_recorder_gauge_node(const hsgn_recorder* R, int32_t k, int32_t* i, int32_t* j, double* x,
+                                                double* y) {
+    if (!R || k < 0 || k >= (int32_t)R->gi.size()) return HSGN_EINVAL;
+    if (i) *i = R->gi[k];
+    if (j) *j = R->gj[k];
+    if (x) *x = R->gx[k];
+    if (y) *y = R->gy[k];
+    return HSGN_OK;
+}
+
+extern "C" hsgn_status hsgn_recorder_gauges(const hsgn_recorder* R, double* t, double* values) {
+    if (!R) return HSGN_EINVAL;
+    if (t) std::copy(R->gauge_t.begin(), R->gauge_t.end(), t);
+    if (values) std::copy(R->gauge_vals.begin(), R->gauge_vals.end(), values);
+    return HSGN_OK;
+}
+
+extern "C" hsgn_status hsgn_recorder_conservation(const hsgn_recorder* R, double* rows4) {
+    if (!R || !rows4) return HSGN_EINVAL;
+    std::copy(R->cons.begin(), R->cons.end(), rows4);
+    return HSGN_OK;
+}
+
+extern "C" hsgn_status hsgn_recorder_snapshot(const hsgn_recorder* R, int32_t k, double* target, double* actual,
+                                              double* host_state) {
+    if (!R || k < 0 || k >= (int32_t)R->snaps.size()) return HSGN_EINVAL;
+    const auto& s = R->snaps[k];
+    if (target) *target = s.target;
+    if (actual) *actual = s.actual;
+    if (host_state) {
+        hsgn_ctx* c = R->c;
+        CK(cudaSetDevice(c->device));
+        CK(cudaStreamSynchronize(c->stream));  // the stream-ordered copy has landed
+        std::memcpy(host_state, s.host, sizeof(double) * 5 * (size_t)c->grid.nx * c->ny_loc);
+    }
     return HSGN_OK;
 }
 

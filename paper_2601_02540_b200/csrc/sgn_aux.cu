@@ -88,6 +88,40 @@ __global__ void __launch_bounds__(256) row_sum_kernel(const AuxArgs A, int kind,
     }
 }
 
+// The recorder's conservation row (io.hpp:137-144) in one pass over q, b and
+// q_t: rows[k*ny + j] for k = 0 mass, 1 energy, 2 energy rate, each with
+// the accumulation order of row_sum_kernel (so bit-identical to it).
+__global__ void __launch_bounds__(256) cons_rows_kernel(const AuxArgs A, const double* q, const double* qt,
+                                                        double* rows) {
+    __shared__ double sh[3][256], sl[3][256];
+    const int j = blockIdx.x;
+    const long long base = (long long)j * A.nx;
+    DD acc[3] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+    for (int i = threadIdx.x; i < A.nx; i += blockDim.x) {
+        const double wx = (A.x_bounded && (i == 0 || i == A.nx - 1)) ? dmul(0.5, A.dx) : A.dx;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) acc[k] = dd_add_d(acc[k], dmul(wx, integrand(k, A, q, qt, 0, base + i)));
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        sh[k][threadIdx.x] = acc[k].hi;
+        sl[k][threadIdx.x] = acc[k].lo;
+    }
+    __syncthreads();
+    if (threadIdx.x < 3) {
+        const int k = threadIdx.x;
+        DD t{0.0, 0.0};
+        for (int m = 0; m < (int)blockDim.x; ++m) t = dd_add(t, DD{sh[k][m], sl[k][m]});
+        rows[(long long)k * A.ny + j] = dadd(t.hi, t.lo);
+    }
+}
+
+// Gauge samples h + b at the recorder's nodes (io.hpp:131-135).
+__global__ void gauge_kernel(const double* h, const double* b, const long long* idx, int n, double* out) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g < n) out[g] = dadd(h[idx[g]], b[idx[g]]);
+}
+
 // Depth pre-check of the standalone rhs() (rhs.hpp:94-97): count !(h > 0).
 __global__ void depth_check_kernel(const double* h, long long n, unsigned long long* bad) {
     unsigned long long c = 0;
@@ -188,6 +222,17 @@ __global__ void init_aux_kernel(const AuxArgs A, double* q) {
 cudaError_t launch_row_sums(const AuxArgs& A, int kind, const double* q, const double* qt, int field,
                             double* rows, cudaStream_t st) {
     row_sum_kernel<<<A.ny, 256, 0, st>>>(A, kind, q, qt, field, rows);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_cons_rows(const AuxArgs& A, const double* q, const double* qt, double* rows, cudaStream_t st) {
+    cons_rows_kernel<<<A.ny, 256, 0, st>>>(A, q, qt, rows);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gauges(const double* h, const double* b, const long long* idx, int n, double* out,
+                          cudaStream_t st) {
+    gauge_kernel<<<(n + 127) / 128, 128, 0, st>>>(h, b, idx, n, out);
     return cudaGetLastError();
 }
 

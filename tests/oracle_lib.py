@@ -122,6 +122,8 @@ class Oracle:
                               C.c_int, C.c_int, G, PH, PD, PD, C.POINTER(C.c_int), PD, PD,
                               C.c_char_p, C.c_int)
             self._rhs_repeat = f("rhs_repeat", C.c_int, G, PH, PD, D, PD, PD, C.c_int)
+            self._run_rec = f("run_recorded", C.c_int, G, PH, PD, C.c_int, PD, D, D, C.POINTER(Cfg), PD,
+                              C.POINTER(Record), C.c_char_p, C.c_int, PD, C.c_int, PD, I64)
         else:
             self._fixed = f("bs3_fixed_steps", C.c_int, G, PH, PD, PD, PD, D, D, C.c_int, C.c_int)
 
@@ -214,6 +216,20 @@ class Oracle:
         return o
 
     # ref-only ----------------------------------------------------------------
+    def run_recorded(self, grid, phys, b, q0, t0, t_final, cfg, out_dir, gauges=(), targets=(), stride=1,
+                     source_kind=0):
+        """adaptive_solve + RunRecorder + flush() (cli.hpp:100-116): the
+        reference writes its CSVs into out_dir.  Returns (q, record)."""
+        q0 = np.ascontiguousarray(q0, dtype=np.float64)
+        out = np.empty_like(q0)
+        rec = Record()
+        g = np.ascontiguousarray(np.asarray(gauges, dtype=np.float64).reshape(-1))
+        tg = np.ascontiguousarray(np.asarray(targets, dtype=np.float64).reshape(-1))
+        self._run_rec(C.byref(grid), C.byref(phys), _p(np.ascontiguousarray(b, np.float64)), source_kind,
+                      _p(q0), t0, t_final, C.byref(cfg), _p(out), C.byref(rec), out_dir.encode(),
+                      len(g) // 2, _p(g) if len(g) else None, len(tg), _p(tg) if len(tg) else None, int(stride))
+        return out, rec
+
     def prepare(self, name: str, nx=0, ny=0, **params):
         """make_scenario + prepare_run; returns (grid, phys, b, q0, source_kind, t0, t_final)."""
         keys = (C.c_char_p * max(1, len(params)))(*[k.encode() for k in params])
