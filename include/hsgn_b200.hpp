@@ -23,7 +23,9 @@
 #include <array>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
+#include <fstream>
 #include <functional>
 #include <limits>
 #include <stdexcept>
@@ -294,17 +296,164 @@ inline void observer_tramp(double t, const hsgn_state* q, const hsgn_state* qt, 
 }
 }  // namespace detail
 
-// adaptive_solve (time_integration.hpp:209-350) on the fused stage kernels.
-inline SolutionRecord adaptive_solve(RhsContext& ctx, const StateField& q0, double t0, double t_final,
-                                     const IntegratorConfig& cfg, const AcceptObserver& on_accept = {}) {
+// ---------------------------------------------------------------- run recorder (io.hpp)
+
+inline std::string fmt17(double v) {  // io.hpp:19-23
+    char buf[40];
+    std::snprintf(buf, sizeof(buf), "%.17g", v);
+    return buf;
+}
+inline std::string fmt_short(double v) {  // io.hpp:26-30
+    char buf[40];
+    std::snprintf(buf, sizeof(buf), "%g", v);
+    return buf;
+}
+
+struct GaugeNode {  // io.hpp:32-35
+    int i = 0, j = 0;
+    double x = 0.0, y = 0.0;
+};
+
+struct SnapshotRecord {  // io.hpp:96-100
+    double target = 0.0;
+    double actual = 0.0;
+    std::string path;
+};
+
+// write_snapshot_csv (io.hpp:50-59)
+inline void write_snapshot_csv(const std::string& path, const Grid2D& grid, const StateField& q, const Field2D& b) {
+    std::ofstream out(path);
+    if (!out) throw std::runtime_error("cannot write '" + path + "'");
+    out << "x,y,h,u,v,w,eta,b\n";
+    for (int j = 0; j < grid.ny; ++j)
+        for (int i = 0; i < grid.nx; ++i)
+            out << fmt17(grid.x(i)) << ',' << fmt17(grid.y(j)) << ',' << fmt17(q.h(i, j)) << ','
+                << fmt17(q.u(i, j)) << ',' << fmt17(q.v(i, j)) << ',' << fmt17(q.w(i, j)) << ','
+                << fmt17(q.eta(i, j)) << ',' << fmt17(b(i, j)) << '\n';
+}
+
+// RunRecorder (io.hpp:107-219) on the device (hsgn_recorder_*): pass it to
+// adaptive_solve instead of wiring on_accept by hand (cli.hpp:100-111).
+// Snapshot CSVs are written when adaptive_solve returns; flush() writes
+// gauges.csv and conservation.csv as the reference does.
+class RunRecorder {
+public:
+    struct ConsRow {
+        double t, mass, energy, energy_rate;
+    };
+
+    RunRecorder(RhsContext& ctx, std::string out_dir, std::vector<std::array<double, 2>> gauge_positions,
+                std::vector<double> snapshot_targets, std::int64_t conservation_stride)
+        : ctx_(ctx), dir_(std::move(out_dir)) {
+        std::vector<double> xy;
+        for (const auto& g : gauge_positions) {
+            xy.push_back(g[0]);
+            xy.push_back(g[1]);
+        }
+        ctx_.check(hsgn_recorder_create(ctx_.handle(), static_cast<int32_t>(gauge_positions.size()),
+                                        xy.empty() ? nullptr : xy.data(),
+                                        static_cast<int32_t>(snapshot_targets.size()),
+                                        snapshot_targets.empty() ? nullptr : snapshot_targets.data(),
+                                        conservation_stride, &r_),
+                   "RunRecorder");
+    }
+    RunRecorder(const RunRecorder&) = delete;
+    RunRecorder& operator=(const RunRecorder&) = delete;
+    ~RunRecorder() { hsgn_recorder_destroy(r_); }
+    hsgn_recorder* handle() const { return r_; }
+
+    std::vector<GaugeNode> gauge_nodes() const {
+        std::vector<GaugeNode> out;
+        GaugeNode n;
+        while (hsgn_recorder_gauge_node(r_, static_cast<int32_t>(out.size()), &n.i, &n.j, &n.x, &n.y) == HSGN_OK)
+            out.push_back(n);
+        return out;
+    }
+    std::vector<ConsRow> conservation_rows() const {
+        int64_t rows = 0;
+        hsgn_recorder_counts(r_, nullptr, &rows, nullptr);
+        std::vector<double> a(4 * rows);
+        if (rows) hsgn_recorder_conservation(r_, a.data());
+        std::vector<ConsRow> out;
+        for (int64_t k = 0; k < rows; ++k) out.push_back({a[4 * k], a[4 * k + 1], a[4 * k + 2], a[4 * k + 3]});
+        return out;
+    }
+    const std::vector<SnapshotRecord>& snapshots() {
+        write_snapshots();
+        return snaps_;
+    }
+
+    // take_snapshot (io.hpp:197-204) for every captured snapshot not on disk yet
+    void write_snapshots() {
+        int32_t n = 0;
+        hsgn_recorder_counts(r_, nullptr, nullptr, &n);
+        const std::size_t np = ctx_.grid.n_total();
+        std::vector<double> buf(5 * np);
+        while (static_cast<int32_t>(snaps_.size()) < n) {
+            SnapshotRecord rec;
+            ctx_.check(hsgn_recorder_snapshot(r_, static_cast<int32_t>(snaps_.size()), &rec.target, &rec.actual,
+                                              buf.data()),
+                       "RunRecorder snapshot");
+            StateField q(ctx_.grid);
+            detail::unpack(buf, q);
+            rec.path = dir_ + "/snapshot_t" + fmt_short(rec.target) + ".csv";
+            write_snapshot_csv(rec.path, ctx_.grid, q, ctx_.phys.b);
+            snaps_.push_back(rec);
+        }
+    }
+
+    // flush (io.hpp:155-185)
+    void flush() {
+        write_snapshots();
+        const std::vector<GaugeNode> nodes = gauge_nodes();
+        if (!nodes.empty()) {
+            const std::string path = dir_ + "/gauges.csv";
+            std::ofstream out(path);
+            if (!out) throw std::runtime_error("cannot write '" + path + "'");
+            for (std::size_t g = 0; g < nodes.size(); ++g)
+                out << "# gauge_" << g + 1 << " at (" << fmt17(nodes[g].x) << ", " << fmt17(nodes[g].y) << ")\n";
+            out << "t";
+            for (std::size_t g = 0; g < nodes.size(); ++g) out << ",gauge_" << g + 1;
+            out << '\n';
+            int64_t rows = 0;
+            hsgn_recorder_counts(r_, &rows, nullptr, nullptr);
+            std::vector<double> t(rows), v(rows * nodes.size());
+            if (rows) hsgn_recorder_gauges(r_, t.data(), v.data());
+            for (int64_t r = 0; r < rows; ++r) {
+                out << fmt17(t[r]);
+                for (std::size_t g = 0; g < nodes.size(); ++g) out << ',' << fmt17(v[r * nodes.size() + g]);
+                out << '\n';
+            }
+        }
+        const std::string path = dir_ + "/conservation.csv";
+        std::ofstream out(path);
+        if (!out) throw std::runtime_error("cannot write '" + path + "'");
+        out << "t,total_mass,total_energy,semidiscrete_energy_rate\n";
+        for (const ConsRow& r : conservation_rows())
+            out << fmt17(r.t) << ',' << fmt17(r.mass) << ',' << fmt17(r.energy) << ',' << fmt17(r.energy_rate)
+                << '\n';
+    }
+
+private:
+    RhsContext& ctx_;
+    std::string dir_;
+    hsgn_recorder* r_ = nullptr;
+    std::vector<SnapshotRecord> snaps_;
+};
+
+namespace detail {
+inline SolutionRecord solve(RhsContext& ctx, const StateField& q0, double t0, double t_final,
+                            const IntegratorConfig& cfg, const AcceptObserver& on_accept, RunRecorder* recorder) {
     hsgn_cfg c{cfg.abs_tol, cfg.rel_tol, cfg.dt_initial, cfg.dt_max,  cfg.safety,
                cfg.growth_cap, cfg.shrink_floor, cfg.max_steps, cfg.fixed_dt, cfg.h_floor};
     ctx.upload(q0, ctx.scratch(0));
     hsgn_record r;
-    detail::ObsBox box{&ctx, &on_accept, StateField(ctx.grid), StateField(ctx.grid)};
-    ctx.check(hsgn_solve(ctx.handle(), ctx.scratch(0), t0, t_final, &c, ctx.scratch(1), &r,
-                         on_accept ? detail::observer_tramp : nullptr, &box),
+    ObsBox box{&ctx, &on_accept, StateField(ctx.grid), StateField(ctx.grid)};
+    ctx.check(hsgn_solve_recorded(ctx.handle(), ctx.scratch(0), t0, t_final, &c, ctx.scratch(1), &r,
+                                  on_accept ? observer_tramp : nullptr, &box,
+                                  recorder ? recorder->handle() : nullptr),
               "adaptive_solve");
+    if (recorder) recorder->write_snapshots();
     SolutionRecord rec;
     rec.q = StateField(ctx.grid);
     ctx.download(ctx.scratch(1), rec.q);
@@ -316,6 +465,20 @@ inline SolutionRecord adaptive_solve(RhsContext& ctx, const StateField& q0, doub
     rec.aborted = r.aborted != 0;
     rec.abort_reason = r.reason;
     return rec;
+}
+}  // namespace detail
+
+// adaptive_solve (time_integration.hpp:209-350) on the fused stage kernels.
+inline SolutionRecord adaptive_solve(RhsContext& ctx, const StateField& q0, double t0, double t_final,
+                                     const IntegratorConfig& cfg, const AcceptObserver& on_accept = {}) {
+    return detail::solve(ctx, q0, t0, t_final, cfg, on_accept, nullptr);
+}
+
+// ... with the on-device RunRecorder as the observer (cmd_run, cli.hpp:100-111).
+inline SolutionRecord adaptive_solve(RhsContext& ctx, const StateField& q0, double t0, double t_final,
+                                     const IntegratorConfig& cfg, RunRecorder& recorder,
+                                     const AcceptObserver& on_accept = {}) {
+    return detail::solve(ctx, q0, t0, t_final, cfg, on_accept, &recorder);
 }
 
 }  // namespace hsgn_b200

@@ -6,7 +6,10 @@
 
 #include <cmath>
 #include <cstdio>
+#include <filesystem>
+#include <fstream>
 #include <random>
+#include <sstream>
 
 using namespace hsgn_b200;
 
@@ -36,6 +39,51 @@ static void randomize(StateField& q, unsigned seed) {  // test_rhs.cpp:22-33
         q.w[k] = vel(rng);
         q.eta[k] = depth(rng);
     }
+}
+
+static std::string slurp(const std::string& p) {
+    std::ifstream in(p);
+    std::stringstream ss;
+    ss << in.rdbuf();
+    return ss.str();
+}
+
+static std::vector<std::vector<double>> csv_rows(const std::string& p) {  // skips '#' lines and the header
+    std::vector<std::vector<double>> rows;
+    std::ifstream in(p);
+    std::string line;
+    bool header = true;
+    while (std::getline(in, line)) {
+        if (line.empty() || line[0] == '#') continue;
+        if (header) {
+            header = false;
+            continue;
+        }
+        std::vector<double> r;
+        std::stringstream ss(line);
+        std::string cell;
+        while (std::getline(ss, cell, ',')) r.push_back(std::stod(cell));
+        rows.push_back(r);
+    }
+    return rows;
+}
+
+// lake_at_rest (scenarios.hpp:480-500) recorded as cmd_run does (cli.hpp:88-116)
+static SolutionRecord run_lake(const std::string& dir, int n, double t_final, std::vector<std::array<double, 2>> gauges,
+                               std::vector<double> snaps, int64_t stride, std::vector<SnapshotRecord>* taken) {
+    std::filesystem::remove_all(dir);
+    std::filesystem::create_directories(dir);
+    Grid2D g = make_grid(-5.0, 5.0, -5.0, 5.0, n, n);
+    RhsContext ctx = context_on(g, 500.0, [](double x, double y) { return 0.1 * std::exp(-0.5 * (x * x + y * y)); });
+    StateField q0(g);
+    for (std::size_t k = 0; k < q0.h.size(); ++k) q0.h[k] = 1.0 - ctx.phys.b[k];
+    q0.eta = q0.h;
+    init_auxiliary(ctx, q0);
+    RunRecorder rec(ctx, dir, gauges, snaps, stride);
+    SolutionRecord sol = adaptive_solve(ctx, q0, 0.0, t_final, IntegratorConfig(), rec);
+    rec.flush();
+    if (taken) *taken = rec.snapshots();
+    return sol;
 }
 
 static double mass_sum(const Grid2D& g, const Field2D& f) {  // sbp.hpp:219-239 weights, plain sum
@@ -156,6 +204,36 @@ int main() {
         SolutionRecord budget = adaptive_solve(ctx, q0, 0.0, 100.0, one);
         CHECK(budget.aborted && budget.abort_reason.find("step budget exhausted") != std::string::npos);
         CHECK(budget.accepted == 1);
+    }
+    {  // run recorder: test_cli.cpp:61-131 ("run command produces the full output set")
+        const std::string dir = "/tmp/hsgn_dropin_run_lake";
+        std::vector<SnapshotRecord> snaps;
+        SolutionRecord sol = run_lake(dir, 20, 1.0, {{0.0, 0.0}}, {0.0, 0.5}, 1, &snaps);
+        CHECK(!sol.aborted && sol.t == 1.0);
+        CHECK(std::filesystem::exists(dir + "/snapshot_t0.csv"));
+        CHECK(std::filesystem::exists(dir + "/snapshot_t0.5.csv"));
+        auto cons = csv_rows(dir + "/conservation.csv");
+        CHECK(cons.size() == static_cast<std::size_t>(sol.accepted) + 1);
+        CHECK(slurp(dir + "/conservation.csv").rfind("t,total_mass,total_energy,semidiscrete_energy_rate\n", 0) == 0);
+        for (const auto& r : cons) {
+            CHECK(std::abs(r[1] - cons[0][1]) <= 1e-12 * std::abs(cons[0][1]));
+            CHECK(std::abs(r[2] - cons[0][2]) <= 1e-12 * std::abs(cons[0][2]));
+            CHECK(std::abs(r[3]) <= 1e-11 * std::abs(cons[0][2]));
+        }
+        auto gauges = csv_rows(dir + "/gauges.csv");
+        CHECK(gauges.size() == cons.size());
+        for (const auto& r : gauges) CHECK(std::abs(r[1] - 1.0) <= 1e-12);
+        CHECK(snaps.size() == 2 && snaps[0].target == 0.0 && snaps[0].actual == 0.0);
+        CHECK(csv_rows(dir + "/snapshot_t0.csv").size() == 20 * 20);
+    }
+    {  // reruns are byte-identical (test_cli.cpp:134-156)
+        const std::string a = "/tmp/hsgn_dropin_rerun_a", b = "/tmp/hsgn_dropin_rerun_b";
+        run_lake(a, 16, 0.5, {{1.0, -1.0}}, {0.25}, 1, nullptr);
+        run_lake(b, 16, 0.5, {{1.0, -1.0}}, {0.25}, 1, nullptr);
+        CHECK(slurp(a + "/conservation.csv") == slurp(b + "/conservation.csv"));
+        CHECK(slurp(a + "/gauges.csv") == slurp(b + "/gauges.csv"));
+        CHECK(!slurp(a + "/snapshot_t0.25.csv").empty());
+        CHECK(slurp(a + "/snapshot_t0.25.csv") == slurp(b + "/snapshot_t0.25.csv"));
     }
     std::printf("%s (%d failures)\n", failures ? "FAILED" : "PASSED", failures);
     return failures ? 1 : 0;
