@@ -37,8 +37,16 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-BYTES_PER_NODE = {"S1": 128, "S2": 168, "S3": 88}
-BYTES_PER_POINT_STAGE = 128                           # 384 B per node per step / 3 stages
+BYTES_PER_NODE = {"S1": 128, "S2": 168, "S3": 88, "S31": 128}  # DESIGN.md sections 2b, 3
+
+
+def step_bytes_per_node(fused: bool, chunk: int = 64) -> float:
+    """Algorithmic HBM bytes per node per step of the fixed-step pipeline:
+    unfused S1 + S2 + S3 = 384; fused chunks of n steps S1 + n S2 +
+    (n-1) S31 + S3 = 296 n + 88."""
+    if not fused:
+        return 384.0
+    return (296.0 * chunk + 88.0) / chunk
 METRIC = "grid-point RK-stage updates/sec on 8192² fp64 grid; achieved HBM GB/s"
 
 
@@ -182,6 +190,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--rows-per-block", type=int, default=0)
+    ap.add_argument("--unfused", action="store_true", help="one kernel per stage (A/B of the S31 fusion)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -211,6 +220,9 @@ def main():
         ctx = S.make_slab_context(g, phys, rank, world, local, dist)
     if args.rows_per_block:
         ctx.set_rows_per_block(args.rows_per_block)
+    if args.unfused:
+        ctx.fused_stages = False
+    fused = ctx.fused_stages and world == 1
     y = ctx.state(q)
     k1 = ctx.state()
     H.rhs(ctx, 0.0, y, k1)
@@ -236,7 +248,14 @@ def main():
     H.api._check(ctx, H.api.N.lib().hsgn_profile_stages(ctx._h, y._h, k1._h, dt, 3, ms3), "profile")
     ms3 = list(ms3)
     names = ["S1", "S2", "S3"]
-    dom = max(range(3), key=lambda k: ms3[k])
+    if fused:  # the steady-state step is S2 + S31
+        m31 = H.api.N.D(0.0)
+        H.api._check(ctx, H.api.N.lib().hsgn_profile_fused(ctx._h, y._h, k1._h, dt, 3, H.api.C.byref(m31)),
+                     "profile_fused")
+        ms3.append(m31.value)
+        names.append("S31")
+    cand = [1, 3] if fused else [0, 1, 2]
+    dom = max(cand, key=lambda k: ms3[k])
     peak, peak_kind = peaks()
     achieved = BYTES_PER_NODE[names[dom]] * points / (ms3[dom] * 1e-3) / 1e9
     traffic = None
@@ -245,10 +264,12 @@ def main():
         with open(tpath) as fh:
             traffic = json.load(fh).get(names[dom])
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "kernel": f"sgn_stage_kernel<{names[dom]}>",
+                "traffic": traffic,
+                "kernel": "sgn_s31_kernel" if names[dom] == "S31" else f"sgn_stage_kernel<{names[dom]}>",
                 "bytes_per_node": BYTES_PER_NODE[names[dom]], "peak_source": peak_kind,
-                "stage_ms": {names[k]: ms3[k] for k in range(3)},
-                "step_gbs": BYTES_PER_POINT_STAGE * 3 * points / (ms / args.steps * 1e-3) / 1e9}
+                "stage_ms": {names[k]: ms3[k] for k in range(len(names))},
+                "step_bytes_per_node": step_bytes_per_node(fused),
+                "step_gbs": step_bytes_per_node(fused) * points / (ms / args.steps * 1e-3) / 1e9}
 
     # end-to-end through the public API with host buffers (pinned)
     e2e = None

@@ -124,6 +124,12 @@ int32_t hsgn_stencil_kind(const hsgn_ctx* ctx);
 hsgn_status hsgn_set_tma(hsgn_ctx* ctx, int32_t on);
 int32_t hsgn_tma_enabled(const hsgn_ctx* ctx);
 
+/* Fixed-step stage fusion: 1 (default) = the fixed-step graphs of a
+ * whole-grid context run stage 3 of step n and stage 1 of step n+1 as one
+ * kernel (bit-identical), 0 = one kernel per stage. */
+hsgn_status hsgn_set_fused_stages(hsgn_ctx* ctx, int32_t on);
+int32_t hsgn_fused_stages(const hsgn_ctx* ctx);
+
 /* ctx.n_evals (rhs.hpp:28,84) */
 int64_t hsgn_n_evals(const hsgn_ctx* ctx);
 
@@ -222,6 +228,10 @@ double hsgn_outer_sum(const hsgn_grid* grid, const double* rows, int32_t j_begin
  * (CUDA events on the context stream; inputs copied, caller state intact). */
 hsgn_status hsgn_profile_stages(hsgn_ctx* ctx, const hsgn_state* y, const hsgn_state* k1, double dt,
                                 int32_t reps, double* ms3);
+
+/* Mean device ms of the fused stage-3 + next-stage-1 kernel over `reps` launches. */
+hsgn_status hsgn_profile_fused(hsgn_ctx* ctx, const hsgn_state* y, const hsgn_state* k1, double dt, int32_t reps,
+                               double* ms);
 
 /* ------------------------------------------------------------ in-process slab group */
 

@@ -79,6 +79,9 @@ def lib() -> C.CDLL:
     f("hsgn_stencil_kind", I32, CTX)
     f("hsgn_set_tma", C.c_int, CTX, I32)
     f("hsgn_tma_enabled", I32, CTX)
+    f("hsgn_set_fused_stages", C.c_int, CTX, I32)
+    f("hsgn_fused_stages", I32, CTX)
+    f("hsgn_profile_fused", C.c_int, CTX, STATE, STATE, D, I32, PD)
     f("hsgn_n_evals", I64, CTX)
     f("hsgn_state_alloc", C.c_int, CTX, PST)
     f("hsgn_state_free", C.c_int, CTX, STATE)
@@ -141,4 +144,5 @@ EXPORTS = [
     "hsgn_group_bs3_fixed_steps", "hsgn_group_reduce",
     "hsgn_recorder_create", "hsgn_recorder_destroy", "hsgn_solve_recorded", "hsgn_recorder_counts",
     "hsgn_recorder_gauge_node", "hsgn_recorder_gauges", "hsgn_recorder_conservation", "hsgn_recorder_snapshot",
+    "hsgn_set_fused_stages", "hsgn_fused_stages", "hsgn_profile_fused",
 ]

@@ -277,6 +277,15 @@ class RhsContext:
     def tma(self, on: bool):
         _check(self, N.lib().hsgn_set_tma(self._h, int(bool(on))), "hsgn_set_tma")
 
+    @property
+    def fused_stages(self) -> bool:
+        """Fixed-step graphs fuse stage 3 with the next step's stage 1."""
+        return bool(N.lib().hsgn_fused_stages(self._h))
+
+    @fused_stages.setter
+    def fused_stages(self, on: bool):
+        _check(self, N.lib().hsgn_set_fused_stages(self._h, int(bool(on))), "set_fused_stages")
+
     def state(self, host=None) -> DeviceState:
         return DeviceState(self, host)
 

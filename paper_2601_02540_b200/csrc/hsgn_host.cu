@@ -130,6 +130,7 @@ struct hsgn_ctx {
     int forced_kind = -1;  // stencil kind override (tests); -1 = automatic
     int use_tma = 0;       // TMA staging of raw inputs when nx is even (opt-in: slower in r1)
     int in_group = 0;      // member of an in-process slab group (halo pulls by the group)
+    int fused = 1;         // fixed-step graphs use the S3+S1 kernel (whole-grid contexts)
     int64_t n_evals = 0;
     std::string err;
     // workspace for the integrator
@@ -144,7 +145,7 @@ struct hsgn_ctx {
     double* d_rows = nullptr;
     double* h_rows = nullptr;
     StepRec* h_rec = nullptr;
-    std::map<std::tuple<int, int, uint64_t, uint64_t, uint64_t>, FixedGraph> graphs;  // (steps, parity, gauges, dt, rpb)
+    std::map<std::tuple<int, int, uint64_t, uint64_t, uint64_t, uint64_t>, FixedGraph> graphs;  // (steps, parity, gauges, dt, rpb, floor)
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     double last_ms = 0.0;
     int64_t last_kernels = 0;
@@ -404,6 +405,18 @@ static hsgn_status enqueue_stage(hsgn_ctx* c, int stage, const hsgn_state* y, co
                                  hsgn_state* ynew, hsgn_state* k4, hsgn_state* part, StepRec* rec,
                                  const StepRec* prev, double t, double dt, bool adaptive, double atol,
                                  double rtol) {
+    if (stage == 31) {  // fused: k4 = f(ynew) of this step, k2 = f(ynew + dt/2 k4) of the next (rec = next's)
+        StageArgs A = stage_args(c, MODE_S31, t + dt);
+        A.a = 0.5 * dt;
+        A.y = ynew->base;
+        A.out = k4->base;
+        A.out2 = k2->base;
+        A.bad = const_cast<unsigned long long*>(&prev->bad[2]);  // the S3 half belongs to the previous step
+        A.bad2 = &rec->bad[0];
+        A.halt = c->d_halt;
+        A.chk_bad = &prev->bad[1];
+        return launch(c, MODE_S31, A);
+    }
     StageArgs A;
     if (stage == 1) {  // k2 = f(t + dt/2, y + (dt/2) k1)
         A = stage_args(c, MODE_S1, t + 0.5 * dt);
@@ -454,7 +467,46 @@ static hsgn_status enqueue_stage(hsgn_ctx* c, int stage, const hsgn_state* y, co
     A.minh = &rec->minh;
     A.halt = c->d_halt;
     A.chk_bad = &rec->bad[0];
+    if (prev && c->fused) {  // after an S31: its S3 half and the floor of the previous step
+        A.chk_bad2 = &prev->bad[2];
+        A.chk_minh = &prev->minh;
+    }
     return launch(c, MODE_S2, A);
+}
+
+// A chunk of `steps` fixed steps from buffer parity `parity` with the fused
+// S3+S1 kernel between steps: S1, S2, (S31, S2) x (steps-1), S3 -- 2 steps+1
+// launches (+1 gauge gather per step with a recorder).  Whole-grid contexts.
+static hsgn_status enqueue_chunk_fused(hsgn_ctx* c, int parity, int steps, double dt, const hsgn_recorder* R,
+                                       int64_t* kernels) {
+    hsgn_state* Y[2] = {&c->ws[0], &c->ws[1]};
+    hsgn_state* K[2] = {&c->ws[2], &c->ws[3]};
+    hsgn_state* k2 = &c->ws[4];
+    const bool gauges = R && !R->gi.empty();
+    hsgn_status st;
+    for (int s = 0; s < steps; ++s) {
+        const int p = (parity + s) & 1;
+        StepRec* rec = &c->d_rec[s];
+        const StepRec* prev = s ? &c->d_rec[s - 1] : nullptr;
+        if (s == 0 && (st = enqueue_stage(c, 1, Y[p], K[p], k2, Y[p ^ 1], K[p ^ 1], nullptr, rec, nullptr, 0.0, dt,
+                                          false, 0, 0)))
+            return st;
+        if ((st = enqueue_stage(c, 2, Y[p], K[p], k2, Y[p ^ 1], K[p ^ 1], nullptr, rec, prev, 0.0, dt, false, 0, 0)))
+            return st;
+        if (gauges) {
+            CK(launch_gauges(Y[p ^ 1]->base, c->b, R->d_idx, (int)R->gi.size(),
+                             R->d_gauge + (size_t)s * R->gi.size(), c->stream));
+            if (kernels) ++*kernels;
+        }
+        if (s + 1 < steps)
+            st = enqueue_stage(c, 31, Y[p], K[p], k2, Y[p ^ 1], K[p ^ 1], nullptr, &c->d_rec[s + 1], rec, 0.0, dt,
+                               false, 0, 0);
+        else
+            st = enqueue_stage(c, 3, Y[p], K[p], k2, Y[p ^ 1], K[p ^ 1], nullptr, rec, prev, 0.0, dt, false, 0, 0);
+        if (st) return st;
+    }
+    if (kernels) *kernels += 2 * steps + 1;
+    return HSGN_OK;
 }
 
 // One fused BS3 step (S1, S2, S3) with the slab halo exchange after each
@@ -716,6 +768,14 @@ hsgn_status hsgn_set_stencil_kind(hsgn_ctx* c, int32_t kind) {
 
 int32_t hsgn_stencil_kind(const hsgn_ctx* c) { return c ? c->base.pow2 : -1; }
 
+hsgn_status hsgn_set_fused_stages(hsgn_ctx* c, int32_t on) {
+    if (!c) return HSGN_EINVAL;
+    c->fused = on ? 1 : 0;
+    return reconfigure(c);
+}
+
+int32_t hsgn_fused_stages(const hsgn_ctx* c) { return c ? c->fused : 0; }
+
 hsgn_status hsgn_set_tma(hsgn_ctx* c, int32_t on) {
     if (!c) return HSGN_EINVAL;
     c->use_tma = on ? 1 : 0;
@@ -878,7 +938,7 @@ hsgn_status get_fixed_graph(hsgn_ctx* c, int steps, int parity, double dt, const
                             FixedGraph** out) {
     const bool gauges = R && !R->gi.empty();
     auto key = std::make_tuple(steps, parity, gauges ? (uint64_t)(uintptr_t)R->d_gauge : 0ull, bits_of(dt),
-                               (uint64_t)c->base.rows_per_block);
+                               (uint64_t)c->base.rows_per_block, bits_of(c->base.h_floor));
     auto it = c->graphs.find(key);
     if (it != c->graphs.end()) {
         *out = &it->second;
@@ -890,7 +950,8 @@ hsgn_status get_fixed_graph(hsgn_ctx* c, int steps, int parity, double dt, const
     CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
     reset_recs(c, steps);
     hsgn_status st = HSGN_OK;
-    for (int s = 0; s < steps && !st; ++s) {
+    if (c->fused && c->nranks == 1) st = enqueue_chunk_fused(c, parity, steps, dt, R, nullptr);
+    for (int s = 0; s < steps && !st && !(c->fused && c->nranks == 1); ++s) {
         const int p = (parity + s) & 1;
         st = enqueue_step(c, Y[p], K[p], &c->ws[4], Y[p ^ 1], K[p ^ 1], nullptr, &c->d_rec[s],
                           s ? &c->d_rec[s - 1] : nullptr, 0.0, dt, false, 0, 0, nullptr);
@@ -932,7 +993,7 @@ static hsgn_status run_fixed_chunk(hsgn_ctx* c, int parity, int steps, double t,
         FixedGraph* fg = nullptr;
         if ((st = get_fixed_graph(c, steps, parity, dt, R, &fg))) return st;
         CK(cudaGraphLaunch(fg->exec, c->stream));
-        if (kernels) *kernels += (gauges ? 4 : 3) * steps;
+        if (kernels) *kernels += (gauges ? steps : 0) + (c->fused ? 2 * steps + 1 : 3 * steps);
     } else {
         hsgn_state* Y[2] = {&c->ws[0], &c->ws[1]};
         hsgn_state* K[2] = {&c->ws[2], &c->ws[3]};
@@ -966,7 +1027,7 @@ static hsgn_status run_fixed_chunk(hsgn_ctx* c, int parity, int steps, double t,
             }
         double mh;
         std::memcpy(&mh, &r.minh, 8);
-        if (r.minh != ~0ull && mh <= c->phys.h_floor) {
+        if (r.minh != ~0ull && mh <= c->base.h_floor) {  // the run's floor (IntegratorConfig::h_floor)
             *done = s;
             *fail_kind = 2;
             return HSGN_OK;
@@ -1090,6 +1151,7 @@ extern "C" hsgn_status hsgn_solve_recorded(hsgn_ctx* c, const hsgn_state* q0, do
     hsgn_status st;
     const int CHUNK = 64;
     if ((st = ensure_ws(c, CHUNK))) return st;
+    c->base.h_floor = cfg->h_floor;  // the stage kernels' halt test and the chunk scan use the run's floor
     auto copy_state = [&](const hsgn_state* src, hsgn_state* dst) -> hsgn_status {
         CK(cudaMemcpyAsync(dst->base - c->grid.nx, src->base - c->grid.nx, sizeof(double) * 5 * c->fs,
                            cudaMemcpyDeviceToDevice, c->stream));
@@ -1438,6 +1500,7 @@ extern "C" hsgn_status hsgn_bs3_fixed_steps(hsgn_ctx* c, hsgn_state* y, hsgn_sta
     hsgn_status st;
     const int CHUNK = 64;
     if ((st = ensure_ws(c, CHUNK))) return st;
+    c->base.h_floor = c->phys.h_floor;
     // y, k1 are caller buffers: run in the workspace pair and copy back
     CK(cudaMemcpyAsync(c->ws[0].base - c->grid.nx, y->base - c->grid.nx, sizeof(double) * 5 * c->fs,
                        cudaMemcpyDeviceToDevice, c->stream));
@@ -1475,6 +1538,11 @@ extern "C" hsgn_status hsgn_bs3_fixed_steps(hsgn_ctx* c, hsgn_state* y, hsgn_sta
         c->n_evals += 3 * (int64_t)done;
         if (fk == 1) {
             result = fail(c, HSGN_EDEPTH, "non-positive depth in fixed-step mode at t = %f", t);
+            break;
+        }
+        if (fk == 2) {
+            result = fail(c, HSGN_EDEPTH, "depth reached the floor %f during the step to t = %f", c->phys.h_floor,
+                          t + dt);
             break;
         }
     }
@@ -1551,6 +1619,45 @@ extern "C" hsgn_status hsgn_profile_stages(hsgn_ctx* c, const hsgn_state* y, con
     }
     for (int k = 0; k < 4; ++k) cudaEventDestroy(ev[k]);
     for (int k = 0; k < 3; ++k) ms3[k] = acc[k] / reps;
+    return HSGN_OK;
+}
+
+// Mean device ms of the fused S3+S1 kernel (S31) over `reps` launches on the
+// ynew of one step from (y, k1) (workspace copies; caller state intact).
+extern "C" hsgn_status hsgn_profile_fused(hsgn_ctx* c, const hsgn_state* y, const hsgn_state* k1, double dt,
+                                          int32_t reps, double* ms) {
+    if (!c || !y || !k1 || !ms || reps < 1) return HSGN_EINVAL;
+    if (c->nranks != 1) return fail(c, HSGN_EINVAL, "the fused kernel needs a whole-grid context");
+    CK(cudaSetDevice(c->device));
+    hsgn_status st;
+    if ((st = ensure_ws(c, 2))) return st;
+    CK(cudaMemcpyAsync(c->ws[0].base - c->grid.nx, y->base - c->grid.nx, sizeof(double) * 5 * c->fs,
+                       cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->ws[2].base - c->grid.nx, k1->base - c->grid.nx, sizeof(double) * 5 * c->fs,
+                       cudaMemcpyDeviceToDevice, c->stream));
+    reset_recs(c, 2);
+    for (int stage = 1; stage <= 2; ++stage)
+        if ((st = enqueue_stage(c, stage, &c->ws[0], &c->ws[2], &c->ws[4], &c->ws[1], &c->ws[3], nullptr,
+                                &c->d_rec[0], nullptr, 0.0, dt, false, 0, 0)))
+            return st;
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    double acc = 0.0;
+    for (int r = 0; r < reps; ++r) {
+        CK(cudaEventRecord(e0, c->stream));
+        if ((st = enqueue_stage(c, 31, &c->ws[0], &c->ws[2], &c->ws[4], &c->ws[1], &c->ws[3], nullptr,
+                                &c->d_rec[1], &c->d_rec[0], 0.0, dt, false, 0, 0)))
+            return st;
+        CK(cudaEventRecord(e1, c->stream));
+        CK(cudaEventSynchronize(e1));
+        float m = 0.f;
+        cudaEventElapsedTime(&m, e0, e1);
+        acc += m;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *ms = acc / reps;
     return HSGN_OK;
 }
 

@@ -29,6 +29,7 @@
 //     rows written by the slab halo exchange.
 #include <cuda_runtime.h>
 
+#include <climits>
 #include <cstdint>
 
 #include "sgn_device.cuh"
@@ -64,6 +65,7 @@ struct KPtrs {
     double* out[5];
     double* part[5];
     const double* yold[5];
+    double* out2[5];  // S31: k2 of the next step
 };
 
 struct Raw {  // raw stage-input data at one node
@@ -105,8 +107,8 @@ __device__ __forceinline__ void load_raw(const KPtrs& P, unsigned off, Raw& r) {
 // q = y + a*k (state_add1, time_integration.hpp:61-75).  Stores the ring
 // pairs of the node (S already offset by ring row and column), fills the
 // y-quantities; returns h > 0.
-template <int MODE>
-__device__ __forceinline__ bool products(const StageArgs& A, const Raw& raw, double2* S, YQ& Y) {
+template <int MODE, bool STORE_RH = true>
+__device__ __forceinline__ bool products(const StageArgs& A, const Raw& raw, double2* S, YQ& Y, double* rh_out = nullptr) {
     double q[5];
 #pragma unroll
     for (int f = 0; f < 5; ++f)
@@ -123,7 +125,8 @@ __device__ __forceinline__ bool products(const StageArgs& A, const Raw& raw, dou
     S[P_VW * BX] = make_double2(v, w);
     S[P_EB * BX] = make_double2(e, b);
     S[P_RHB * BX] = make_double2(r, hpb);
-    S[P_RH * BX] = make_double2(rh, 0.0);
+    if (STORE_RH) S[P_RH * BX] = make_double2(rh, 0.0);
+    if (rh_out) *rh_out = rh;
     if (MODE == MODE_S2) {  // ((y + c1 k1) + c2 k2): the k3-free part of ynew (state_add3)
         double yp[5];
 #pragma unroll
@@ -399,66 +402,25 @@ __device__ __forceinline__ void neighbour_y(const double2* S, YQ& Y) {
     Y.hvw = dmul(Y.hv, Y.w);
 }
 
-// One row of the march: form row jn = j+1 (ring slot SN, register set yn),
-// then finish row j (ring slot SC; row j-1 is register set yp).
-template <int MODE, int KIND, bool TMA, int SC>
-__device__ __forceinline__ void march_row(const StageArgs& A, const KPtrs& P, Thr& T, double2* ring, double* rawring,
-                                          unsigned long long* bars, int j0, int j, const YQ& yp, YQ& yn, Raw& raw,
-                                          Raw& raw_next) {
-    constexpr int NP = npairs<MODE>();
-    constexpr int SN = (SC + 1) % 3;
-    const int jn = j + 1;
-    const unsigned nx = (unsigned)A.nx;
-    // register prefetch of raw(jn+1), issued after products(jn) so the load is
-    // in flight during the finish of row j.  (Issuing it before products(jn)
-    // needs two raw register sets and a 6x-unrolled march: measured slower in
-    // round 1 -- spills in S1/S2, I-cache in S3 -- so EARLY stays off; raw and
-    // raw_next may then alias.)
-    constexpr bool EARLY = HSGN_EARLY_PF && nraw<MODE>() <= 6;
-    if (!TMA && EARLY && jn < T.j1) load_raw<MODE>(P, (unsigned)map_row(A, jn + 1) * nx + T.col, raw_next);
-    if (!TMA && HSGN_L2_PF > 1 && jn + HSGN_L2_PF <= T.j1) l2_prefetch_row<MODE>(A, T, jn + HSGN_L2_PF);
-    if (TMA) {  // raw row jn lives in raw slot (SC+2)%3; row j+3 goes into slot (SC+1)%3
-        constexpr int RS = (SC + 2) % 3, RI = (SC + 1) % 3;
-        mbar_wait(&bars[RS], (unsigned)(((jn - j0 + 1) / 3) & 1));
-        raw_from_smem<MODE>(rawring + RS * (nraw<MODE>() * RW), T.tid, raw);
-        if (T.tid == 0 && j + 3 <= T.j1)
-            tma_issue_row<MODE>(A, P, j + 3, (int)blockIdx.x * WX, rawring + RI * (nraw<MODE>() * RW), &bars[RI]);
-    }
-    {  // products of row jn (for D_y of row j, and D_x of row jn one step later)
-        const bool ok = products<MODE>(A, raw, ring + SN * (NP * BX) + T.tid, yn);
-        if (T.finish && jn < T.j1 && !ok) ++T.bad;
-    }
-    if (!TMA && !EARLY && jn < T.j1) load_raw<MODE>(P, (unsigned)map_row(A, jn + 1) * nx + T.col, raw);
-    if (!TMA && EARLY) raw = raw_next;  // (register moves: the 3x unroll cannot alternate two sets)
-    // One barrier per row: row j's ring entries (written one step ago) become
-    // visible, and this step's writes to slot SN are ordered after the last
-    // reads of that slot (finish of row j-2, before the previous barrier).
-    __syncthreads();
-    if (!T.finish) return;
-
-    const double2* S = ring + SC * (NP * BX);
-    const double2* Sc = S + T.tid;  // row j, own column
-    const double cx = T.cx;
-    const double cy = (j == T.jc0 || j == T.jc1) ? A.c1y : A.cpy;
+// The combine pass (rhs.hpp:147-213, wall SAT sbp.hpp:272-284, source
+// rhs.hpp:212-213) at one node of row j.  S: ring slot of row j (centre at
+// S + tid, x-neighbours at S + sl / S + sr); ypr / ynr: the y-quantities of
+// rows j-1 / j+1 at this column.  All stage kernels share it.
+template <int KIND>
+__device__ __forceinline__ void tendency(const StageArgs& A, const double2* S, int tid, int sl, int sr, double cx,
+                                         double cy, bool xl, bool xr, int i, int j, const YQ& ypr, const YQ& ynr,
+                                         double rh, double o[5]) {
+    const double2* Sc = S + tid;  // row j, own column
     // centre values of row j (products re-formed as in rhs.hpp:99-109)
     const double2 c0 = Sc[P_HU * BX], c1 = Sc[P_VW * BX], c2 = Sc[P_EB * BX], c3 = Sc[P_RHB * BX];
     const double h = c0.x, u = c0.y, v = c1.x, w = c1.y, b = c2.y, r = c3.x, hpb = c3.y;
-    const double rh = Sc[P_RH * BX].x;
     const double hu = dmul(h, u), u2 = dmul(u, u), hv = dmul(h, v), v2 = dmul(v, v);
     // x-neighbours i-1, i+1
     XQ L, R;
-    neighbour_x(S + T.sl, L);
-    neighbour_x(S + T.sr, R);
+    neighbour_x(S + sl, L);
+    neighbour_x(S + sr, R);
 #define DX(f) const double d##f##_x = sbp_d<KIND>(cx, L.f, R.f)
-    // Row j-1: S1/S3/RHS re-form it from its ring entry (slot SP, own
-    // column), which frees the carried window's registers (96 instead of
-    // ~160) for 6 DMUL + 4 LDS.128 per node; S2 keeps the register window
-    // (measured faster for S2, r1: 2.05 vs 2.95 ms).
-    constexpr bool ywin_smem = HSGN_YWIN_SMEM && MODE != MODE_S2;
-    YQ yprev;
-    if (ywin_smem) neighbour_y(ring + ((SC + 2) % 3) * (NP * BX) + T.tid, yprev);
-    const YQ& ypr = ywin_smem ? yprev : yp;
-#define DY(f) const double d##f##_y = sbp_d<KIND>(cy, ypr.f, yn.f)
+#define DY(f) const double d##f##_y = sbp_d<KIND>(cy, ypr.f, ynr.f)
     DX(h); DX(u); DX(v); DX(w); DX(e); DX(b); DX(hhb); DX(u2); DX(hu); DX(huv); DX(e2h); DX(huw);
     DY(h); DY(u); DY(v); DY(w); DY(e); DY(b); DY(hhb); DY(v2); DY(hv); DY(huv); DY(e2h); DY(hvw);
 #undef DX
@@ -469,14 +431,13 @@ __device__ __forceinline__ void march_row(const StageArgs& A, const KPtrs& P, Th
     auto sc = [&](double x) { return KIND == 2 ? dmul(A.cpx, x) : x; };
     // s + 0.5*G as one rounding: 0.5*G is exact, so fma(0.5, G, s) == RN(s + RN(0.5 G))
     auto add_half = [](double s, double G) { return __fma_rn(0.5, G, s); };
-    double o[5];
     {  // continuity (rhs.hpp:156-157) + wall SAT (sbp.hpp:272-284)
         const double s = sc(dadd(dadd(dadd(dmul(u, dh_x), dmul(h, du_x)), dmul(v, dh_y)), dmul(h, dv_y)));
         double ht = -s;
         if (A.walls) {
             double sat = 0.0;
-            if (T.xl) sat = dsub(sat, dmul(A.tdx, hu));
-            if (T.xr) sat = dadd(sat, dmul(A.tdx, hu));
+            if (xl) sat = dsub(sat, dmul(A.tdx, hu));
+            if (xr) sat = dadd(sat, dmul(A.tdx, hu));
             if (j == 0 && A.sat_y_lo) sat = dsub(sat, dmul(A.tdy, hv));
             if (j == A.ny - 1 && A.sat_y_hi) sat = dadd(sat, dmul(A.tdy, hv));
             ht = dadd(ht, sat);
@@ -536,13 +497,65 @@ __device__ __forceinline__ void march_row(const StageArgs& A, const KPtrs& P, Th
         o[4] = 0.0;
     }
     if (A.source) {  // add_manufactured_sources: after assembly (rhs.hpp:212-213)
-        const double xg = dadd(A.x_min, dmul((double)T.i, A.dx));
+        const double xg = dadd(A.x_min, dmul((double)i, A.dx));
         const double yg = dadd(A.y_min, dmul((double)(A.j_global0 + j), A.dy));
         double s5[5];
         mms_source(A.t, xg, yg, A.g, s5);
 #pragma unroll
         for (int f = 0; f < 5; ++f) o[f] = dadd(o[f], s5[f]);
     }
+}
+
+// One row of the march: form row jn = j+1 (ring slot SN, register set yn),
+// then finish row j (ring slot SC; row j-1 is register set yp).
+template <int MODE, int KIND, bool TMA, int SC>
+__device__ __forceinline__ void march_row(const StageArgs& A, const KPtrs& P, Thr& T, double2* ring, double* rawring,
+                                          unsigned long long* bars, int j0, int j, const YQ& yp, YQ& yn, Raw& raw,
+                                          Raw& raw_next) {
+    constexpr int NP = npairs<MODE>();
+    constexpr int SN = (SC + 1) % 3;
+    const int jn = j + 1;
+    const unsigned nx = (unsigned)A.nx;
+    // register prefetch of raw(jn+1), issued after products(jn) so the load is
+    // in flight during the finish of row j.  (Issuing it before products(jn)
+    // needs two raw register sets and a 6x-unrolled march: measured slower in
+    // round 1 -- spills in S1/S2, I-cache in S3 -- so EARLY stays off; raw and
+    // raw_next may then alias.)
+    constexpr bool EARLY = HSGN_EARLY_PF && nraw<MODE>() <= 6;
+    if (!TMA && EARLY && jn < T.j1) load_raw<MODE>(P, (unsigned)map_row(A, jn + 1) * nx + T.col, raw_next);
+    if (!TMA && HSGN_L2_PF > 1 && jn + HSGN_L2_PF <= T.j1) l2_prefetch_row<MODE>(A, T, jn + HSGN_L2_PF);
+    if (TMA) {  // raw row jn lives in raw slot (SC+2)%3; row j+3 goes into slot (SC+1)%3
+        constexpr int RS = (SC + 2) % 3, RI = (SC + 1) % 3;
+        mbar_wait(&bars[RS], (unsigned)(((jn - j0 + 1) / 3) & 1));
+        raw_from_smem<MODE>(rawring + RS * (nraw<MODE>() * RW), T.tid, raw);
+        if (T.tid == 0 && j + 3 <= T.j1)
+            tma_issue_row<MODE>(A, P, j + 3, (int)blockIdx.x * WX, rawring + RI * (nraw<MODE>() * RW), &bars[RI]);
+    }
+    {  // products of row jn (for D_y of row j, and D_x of row jn one step later)
+        const bool ok = products<MODE>(A, raw, ring + SN * (NP * BX) + T.tid, yn);
+        if (T.finish && jn < T.j1 && !ok) ++T.bad;
+    }
+    if (!TMA && !EARLY && jn < T.j1) load_raw<MODE>(P, (unsigned)map_row(A, jn + 1) * nx + T.col, raw);
+    if (!TMA && EARLY) raw = raw_next;  // (register moves: the 3x unroll cannot alternate two sets)
+    // One barrier per row: row j's ring entries (written one step ago) become
+    // visible, and this step's writes to slot SN are ordered after the last
+    // reads of that slot (finish of row j-2, before the previous barrier).
+    __syncthreads();
+    if (!T.finish) return;
+
+    const double2* S = ring + SC * (NP * BX);
+    const double2* Sc = S + T.tid;  // row j, own column
+    const double cy = (j == T.jc0 || j == T.jc1) ? A.c1y : A.cpy;
+    // Row j-1: S1/S3/RHS re-form it from its ring entry (slot SP, own
+    // column), which frees the carried window's registers (96 instead of
+    // ~160) for 6 DMUL + 4 LDS.128 per node; S2 keeps the register window
+    // (measured faster for S2, r1: 2.05 vs 2.95 ms).
+    constexpr bool ywin_smem = HSGN_YWIN_SMEM && MODE != MODE_S2;
+    YQ yprev;
+    if (ywin_smem) neighbour_y(ring + ((SC + 2) % 3) * (NP * BX) + T.tid, yprev);
+    const YQ& ypr = ywin_smem ? yprev : yp;
+    double o[5];
+    tendency<KIND>(A, S, T.tid, T.sl, T.sr, T.cx, cy, T.xl, T.xr, T.i, j, ypr, yn, Sc[P_RH * BX].x, o);
     // ---- epilogue
     const unsigned off = (unsigned)(j + 1) * nx + T.col;  // bases point at row -1
     if (MODE == MODE_S2) {
@@ -585,6 +598,7 @@ __global__ void __launch_bounds__(BX, min_blocks<MODE>()) sgn_stage_kernel(const
         if (tid == 0) {
             int skip = *A.halt;
             if (!skip && A.chk_bad && *A.chk_bad) skip = 1;
+            if (!skip && A.chk_bad2 && *A.chk_bad2) skip = 1;
             if (!skip && A.chk_minh) {
                 const unsigned long long mb = *A.chk_minh;
                 if (mb != ~0ull && __longlong_as_double((long long)mb) <= A.h_floor) skip = 1;
@@ -709,6 +723,205 @@ __global__ void __launch_bounds__(BX, min_blocks<MODE>()) sgn_stage_kernel(const
     }
 }
 
+// ------------------------------------------------------------ fused S3 + S1
+// Stage 3 of step n and stage 1 of step n+1 in one pass (fixed step, FSAL:
+// y' = ynew, k1' = k4):  k4 = f(ynew), k2' = f(ynew + a k4).  The S3 half
+// runs one row and one column ahead of the S1 half inside the CTA, so the
+// stage-1 input at every stencil point comes from registers/shared memory
+// instead of a second HBM pass: per step the fixed-step pipeline moves
+// 168 (S2) + 128 (S31) = 296 B/node instead of 384.  Arithmetic is the
+// unfused S3 and S1 operation for operation (bit-identical).
+//
+//   * tile: BX threads, columns i0-2 .. i0+BX-3; the S3 half finishes
+//     threads 1..BX-2, the S1 half threads 2..BX-3 (WX2 = BX-4 columns);
+//   * rows: the S1 half finishes rows [j0, j1) of the CTA; the S3 half
+//     rows j0-1 .. j1 (k4 stored for [j0, j1) only); ynew rows j0-2 .. j1+1;
+//   * two 3-slot rings of 4 pairs (S3 inputs, S1 inputs; the centre 1/h of
+//     each ring row is carried in registers instead), one barrier per row:
+//     49 KB per CTA, 4 CTAs per SM;
+//   * whole-grid contexts only (y edges WRAP or CLAMP: rows -2 and ny+1
+//     exist by wrap/clamp, no ghost rows needed).
+constexpr int WX2 = BX - 4;
+constexpr int NPF = 4;  // ring pairs of the fused kernel (no P_RH)
+
+__device__ __forceinline__ int map_row2(const StageArgs& A, int jr) {
+    if (jr < 0) return A.y_lo == YE_WRAP ? jr + A.ny + 1 : 1;
+    if (jr >= A.ny) return A.y_hi == YE_WRAP ? jr - A.ny + 1 : A.ny;
+    return jr + 1;
+}
+
+struct Thr2 {
+    int tid, i, j0, j1, jc0, jc1;
+    bool fa, fb;  // finishes the S3 half / the S1 half (and owns the column)
+    bool xl, xr;
+    unsigned col;
+    double cx;
+    int sl, sr;
+    unsigned long long bad_a, bad_b;
+};
+
+// S3 half at row r from ring-A slots (ap: row r-1, ac: row r, an: row r+1;
+// rh: 1/h of row r at this column): k4 (stored when owned) and the S1-half
+// input products of row r into ring-B slot bo (its 1/h into *rh_b).
+template <int KIND>
+__device__ __forceinline__ void s31_half3(const StageArgs& A, const KPtrs& P, Thr2& T, const double2* ap,
+                                          const double2* ac, const double2* an, double rh, double2* bo,
+                                          double* rh_b, int r) {
+    if (!T.fa) return;
+    YQ yp, yn;
+    neighbour_y(ap + T.tid, yp);
+    neighbour_y(an + T.tid, yn);
+    const double cy = (r == T.jc0 || r == T.jc1) ? A.c1y : A.cpy;
+    double o[5];
+    tendency<KIND>(A, ac, T.tid, T.sl, T.sr, T.cx, cy, T.xl, T.xr, T.i, r, yp, yn, rh, o);
+    const bool own = T.fb && r >= T.j0 && r < T.j1;
+    if (own) {
+        const unsigned off = (unsigned)(r + 1) * (unsigned)A.nx + T.col;
+#pragma unroll
+        for (int f = 0; f < 5; ++f) P.out[f][off] = o[f];
+    }
+    // next step's stage-1 input ynew + a k4 (state_add1) and its products
+    const double2* Sc = ac + T.tid;
+    const double2 p0 = Sc[P_HU * BX], p1 = Sc[P_VW * BX], p2 = Sc[P_EB * BX];
+    Raw rb;
+    rb.y[0] = p0.x;
+    rb.y[1] = p0.y;
+    rb.y[2] = p1.x;
+    rb.y[3] = p1.y;
+    rb.y[4] = p2.x;
+    rb.b = p2.y;
+#pragma unroll
+    for (int f = 0; f < 5; ++f) rb.k[f] = o[f];
+    YQ unused;
+    const bool ok = products<MODE_S1, false>(A, rb, bo + T.tid, unused, rh_b);
+    if (own && !ok) ++T.bad_b;
+}
+
+// S1 half at row j from ring-B slots (bp: row j-1, bc: row j, bn: row j+1).
+template <int KIND>
+__device__ __forceinline__ void s31_half1(const StageArgs& A, const KPtrs& P, const Thr2& T, const double2* bp,
+                                          const double2* bc, const double2* bn, double rh, int j) {
+    if (!T.fb) return;
+    // a clamped (wall) row reads itself in place of the missing neighbour,
+    // exactly the clamped stage input the unfused S1 forms there
+    if (j == 0 && A.y_lo == YE_CLAMP) bp = bc;
+    if (j == A.ny - 1 && A.y_hi == YE_CLAMP) bn = bc;
+    YQ yp, yn;
+    neighbour_y(bp + T.tid, yp);
+    neighbour_y(bn + T.tid, yn);
+    const double cy = (j == T.jc0 || j == T.jc1) ? A.c1y : A.cpy;
+    double o[5];
+    tendency<KIND>(A, bc, T.tid, T.sl, T.sr, T.cx, cy, T.xl, T.xr, T.i, j, yp, yn, rh, o);
+    const unsigned off = (unsigned)(j + 1) * (unsigned)A.nx + T.col;
+#pragma unroll
+    for (int f = 0; f < 5; ++f) P.out2[f][off] = o[f];
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(BX, 4) sgn_s31_kernel(const StageArgs A, const KPtrs P) {
+    extern __shared__ __align__(16) double2 ring[];  // ring A | ring B, each 3 x NPF x BX
+    __shared__ int s_skip;
+    const int tid = threadIdx.x;
+    if (A.halt) {  // failure protocol
+        if (tid == 0) {
+            int skip = *A.halt;
+            if (!skip && A.chk_bad && *A.chk_bad) skip = 1;
+            if (!skip && A.chk_minh) {
+                const unsigned long long mb = *A.chk_minh;
+                if (mb != ~0ull && __longlong_as_double((long long)mb) <= A.h_floor) skip = 1;
+            }
+            if (skip) *A.halt = 1;
+            s_skip = skip;
+        }
+        __syncthreads();
+        if (s_skip) return;
+    }
+    const int nx = A.nx, ny = A.ny;
+    Thr2 T;
+    T.tid = tid;
+    const int i = (int)blockIdx.x * WX2 - 2 + tid;
+    T.i = i;
+    T.fb = tid >= 2 && tid <= BX - 3 && i >= 0 && i < nx;
+    T.fa = tid >= 1 && tid <= BX - 2 && i >= -1 && i <= nx;
+    int col = i;
+    if (i < 0) col = A.x_bounded ? 0 : nx + i;
+    if (i >= nx) col = (A.x_bounded || i > nx + 1) ? nx - 1 : i - nx;
+    T.col = (unsigned)col;
+    T.xl = A.x_bounded && i == 0;
+    T.xr = A.x_bounded && i == nx - 1;
+    T.cx = (T.xl || T.xr) ? A.c1x : A.cpx;
+    T.sl = T.xl ? tid : tid - 1;
+    T.sr = T.xr ? tid : tid + 1;
+    T.j0 = blockIdx.y * A.rows_per_block;
+    T.j1 = min(ny, T.j0 + A.rows_per_block);
+    T.jc0 = A.y_lo == YE_CLAMP ? 0 : INT_MIN;
+    T.jc1 = A.y_hi == YE_CLAMP ? ny - 1 : INT_MIN;
+    T.bad_a = 0;
+    T.bad_b = 0;
+    const int j0 = T.j0;
+    const unsigned unx = (unsigned)nx;
+    constexpr int SLOT = NPF * BX;
+    // rotating slot pointers (the march is not unrolled: one copy of each
+    // half keeps the kernel inside the instruction cache)
+    double2* a0 = ring;             // ring A: rows j, j+1, j+2 at the top of iteration j
+    double2* a1 = ring + SLOT;
+    double2* a2 = ring + 2 * SLOT;
+    double2* b0 = ring + 3 * SLOT;  // ring B: rows j-1, j, j+1
+    double2* b1 = ring + 4 * SLOT;
+    double2* b2 = ring + 5 * SLOT;
+    double rha1, rha2, rhb1, rhb2;  // 1/h carried: ring A rows j+1, j+2; ring B rows j, j+1
+
+    // ---- prologue: ynew rows j0-2 -> a1, j0-1 -> a2, j0 -> a0; S3 half of
+    // row j0-1 (-> b0); row j0+1 -> a1; S3 half of row j0 (-> b1).  The
+    // pointers then sit as iteration j0 expects.
+    Raw raw;
+    YQ unused;
+    double rh_m2, rh_m1, rh_0, rhb0;
+    load_raw<MODE_S3>(P, (unsigned)map_row2(A, j0 - 2) * unx + T.col, raw);
+    products<MODE_S3, false>(A, raw, a1 + tid, unused, &rh_m2);
+    load_raw<MODE_S3>(P, (unsigned)map_row2(A, j0 - 1) * unx + T.col, raw);
+    products<MODE_S3, false>(A, raw, a2 + tid, unused, &rh_m1);
+    load_raw<MODE_S3>(P, (unsigned)map_row2(A, j0) * unx + T.col, raw);
+    if (!products<MODE_S3, false>(A, raw, a0 + tid, unused, &rh_0) && T.fb) ++T.bad_a;
+    load_raw<MODE_S3>(P, (unsigned)map_row2(A, j0 + 1) * unx + T.col, raw);
+    __syncthreads();
+    // S3 half of row j0-1 (ring B row j0-1 -> b0)
+    s31_half3<KIND>(A, P, T, a1, a2, a0, rh_m1, b0, &rhb0, j0 - 1);
+    // row j0+1 overwrites row j0-2's slot (a1): only this thread's own column
+    // of row j0-2 was read (y-window of the S3 half above)
+    if (!products<MODE_S3, false>(A, raw, a1 + tid, unused, &rha1) && T.fb && j0 + 1 < T.j1) ++T.bad_a;
+    load_raw<MODE_S3>(P, (unsigned)map_row2(A, j0 + 2) * unx + T.col, raw);
+    // S3 half of row j0 (ring B row j0 -> b1)
+    s31_half3<KIND>(A, P, T, a2, a0, a1, rh_0, b1, &rhb1, j0);
+    __syncthreads();  // ring A row j0-1 (a2) is overwritten next; ring B rows j0-1, j0 published
+
+#pragma unroll 1
+    for (int j = j0; j < T.j1; ++j) {
+        // ynew row j+2 into the slot of row j-1 (a2), last read across
+        // threads by the S3 half of row j-1 before the previous barrier
+        if (!products<MODE_S3, false>(A, raw, a2 + tid, unused, &rha2) && T.fb && j + 2 < T.j1) ++T.bad_a;
+        if (j + 1 < T.j1) load_raw<MODE_S3>(P, (unsigned)map_row2(A, j + 3) * unx + T.col, raw);
+        __syncthreads();
+        // S3 half of row j+1 -> ring B row j+1 into the slot of row j-2 (b2),
+        // last read across threads by the S1 half of row j-2
+        s31_half3<KIND>(A, P, T, a0, a1, a2, rha1, b2, &rhb2, j + 1);
+        s31_half1<KIND>(A, P, T, b0, b1, b2, rhb1, j);
+        // rotate: A rows (j+1, j+2, j) -> (a0, a1, a2); B rows (j, j+1, j-1) -> (b0, b1, b2)
+        double2* t = a0;
+        a0 = a1;
+        a1 = a2;
+        a2 = t;
+        t = b0;
+        b0 = b1;
+        b1 = b2;
+        b2 = t;
+        rha1 = rha2;
+        rhb1 = rhb2;
+    }
+    if (T.bad_a) atomicAdd(A.bad, T.bad_a);
+    if (T.bad_b) atomicAdd(A.bad2, T.bad_b);
+}
+
 // Deterministic final sum of per-block partials (single CTA, fixed order,
 // compensated); result goes to out[0].
 __global__ void __launch_bounds__(256) sum_partials_kernel(const double* part, int n, double* out) {
@@ -773,6 +986,7 @@ static cudaError_t launch_mode(const StageArgs& A, cudaStream_t st) {
         P.out[f] = A.out ? A.out + f * A.fs - g : nullptr;
         P.part[f] = A.part ? A.part + f * A.fs - g : nullptr;
         P.yold[f] = A.yold ? A.yold + f * A.fs - g : nullptr;
+        P.out2[f] = A.out2 ? A.out2 + f * A.fs - g : nullptr;
     }
     P.b = A.b - g;
     // TMA staging needs 16-byte aligned row pieces: nx even (host decides)
@@ -781,8 +995,34 @@ static cudaError_t launch_mode(const StageArgs& A, cudaStream_t st) {
 }
 
 template <int KIND>
+static cudaError_t launch_s31(const StageArgs& A, cudaStream_t st) {
+    constexpr size_t bytes = sizeof(double2) * 2 * 3 * NPF * BX;
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e =
+            cudaFuncSetAttribute(sgn_s31_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    KPtrs P;
+    const long long g = A.nx;
+    for (int f = 0; f < 5; ++f) {
+        P.y[f] = A.y + f * A.fs - g;
+        P.k[f] = P.kc[f] = P.yold[f] = nullptr;
+        P.part[f] = nullptr;
+        P.out[f] = A.out + f * A.fs - g;
+        P.out2[f] = A.out2 + f * A.fs - g;
+    }
+    P.b = A.b - g;
+    dim3 grid((A.nx + WX2 - 1) / WX2, (A.ny + A.rows_per_block - 1) / A.rows_per_block);
+    sgn_s31_kernel<KIND><<<grid, BX, bytes, st>>>(A, P);
+    return cudaGetLastError();
+}
+
+template <int KIND>
 static cudaError_t launch_kind(int mode, const StageArgs& A, cudaStream_t st) {
     switch (mode) {
+        case MODE_S31: return launch_s31<KIND>(A, st);
         case MODE_RHS: return launch_mode<MODE_RHS, KIND>(A, st);
         case MODE_S1: return launch_mode<MODE_S1, KIND>(A, st);
         case MODE_S2: return launch_mode<MODE_S2, KIND>(A, st);

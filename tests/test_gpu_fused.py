@@ -1,0 +1,106 @@
+"""GPU: the fused stage-3 + next-stage-1 kernel (S31).
+
+The fixed-step graphs of a whole-grid context run S1, S2, (S31, S2)...,
+S3.  S31 must reproduce the unfused S3 and S1 bit for bit, including at
+the tile seams (124 finished columns per CTA, two halo columns each side),
+the CTA row seams (the S3 half re-runs one row above and below each strip)
+and the wrap / clamp rows, and it must keep the reference's failure
+semantics (which stage of which step failed, the abort reason, the ledger
+and the last valid state).
+"""
+import numpy as np
+import pytest
+
+from oracle_lib import Oracle, Phys, default_cfg, make_grid as omake_grid, mms_exact_field
+
+pytestmark = pytest.mark.gpu
+
+import paper_2601_02540_b200 as H  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def orc():
+    o = Oracle("orc")
+    o.set_threads(8)
+    return o
+
+
+def _ctx(og, b, lam=500.0):
+    g = H.make_grid(og.x_min, og.x_max, og.y_min, og.y_max, og.nx, og.ny, og.kind_x, og.kind_y)
+    return g, H.make_rhs_context(g, H.PhysSetup(9.81, lam, 1e-12, b.reshape(og.ny, og.nx)))
+
+
+def _neq(a, b):
+    return int(np.count_nonzero(np.asarray(a) != np.asarray(b)))
+
+
+@pytest.mark.parametrize("nx,ny,kx,ky,rpb", [
+    (64, 48, 0, 0, 0), (123, 9, 0, 0, 2), (124, 7, 0, 0, 3), (125, 11, 0, 0, 1), (126, 8, 1, 1, 4),
+    (248, 6, 0, 1, 5), (249, 13, 1, 0, 0), (300, 21, 1, 1, 7), (4, 4, 0, 0, 0), (5, 6, 1, 1, 1),
+    (128, 128, 0, 0, 0), (129, 65, 1, 1, 0), (256, 5, 0, 0, 2)])
+def test_fused_fixed_steps_bitwise(orc, nx, ny, kx, ky, rpb):
+    og = omake_grid(nx, ny, kind_x=kx, kind_y=ky)
+    q, b = mms_exact_field(og, 0.3)
+    dx = 2.0 / (nx - 1 if kx else nx)
+    dt = 0.25 * dx / 20.0
+    T = 9 * dt
+    want, rec = orc.solve(og, Phys(9.81, 500.0, 1e-12), b, q, 0.0, T, default_cfg(fixed_dt=dt))
+    g, ctx = _ctx(og, b)
+    if rpb:
+        ctx.set_rows_per_block(rpb)
+    assert ctx.fused_stages
+    res = H.adaptive_solve(ctx, H.StateField(g, q), 0.0, T, H.IntegratorConfig(fixed_dt=dt))
+    assert (res.accepted, res.rhs_evals, res.aborted) == (rec.accepted, rec.rhs_evals, bool(rec.aborted))
+    assert _neq(res.q.flat(), want) == 0
+    ctx.fused_stages = False
+    res2 = H.adaptive_solve(ctx, H.StateField(g, q), 0.0, T, H.IntegratorConfig(fixed_dt=dt))
+    assert _neq(res2.q.flat(), want) == 0
+
+
+def _drying_state(nx, ny, amp, U):
+    x = -1 + np.arange(nx) * 2 / nx
+    y = -1 + np.arange(ny) * 2 / ny
+    X, Y = np.meshgrid(x, y)
+    e = np.exp(-(X ** 2 + Y ** 2) / 0.05)
+    h = 1 - amp * e
+    return np.concatenate([h.ravel(), (U * X * e).ravel(), (U * Y * e).ravel(), np.zeros(nx * ny), h.ravel()])
+
+
+# (amp, U, dt, h_floor): failures at stage 1, at stage 3 (the S3 half of an
+# S31 launch), at the depth floor, and a floor hit on the first step
+@pytest.mark.parametrize("amp,U,dt,floor", [(0.99, 10.0, 1e-3, 1e-12), (0.99, 30.0, 1e-3, 1e-12),
+                                             (0.99, 10.0, 1e-3, 0.005), (0.999, 10.0, 1e-3, 0.005),
+                                             (0.99, 10.0, 3e-3, 1e-12)])
+@pytest.mark.parametrize("fused", [True, False])
+def test_fixed_step_failures_match_reference(orc, amp, U, dt, floor, fused):
+    nx, ny = 64, 48
+    og = omake_grid(nx, ny)
+    q = _drying_state(nx, ny, amp, U)
+    b = np.zeros(nx * ny)
+    want, rec = orc.solve(og, Phys(9.81, 500.0, 1e-12), b, q, 0.0, 200 * dt,
+                          default_cfg(fixed_dt=dt, h_floor=floor))
+    assert rec.aborted
+    g, ctx = _ctx(og, b)
+    ctx.fused_stages = fused
+    res = H.adaptive_solve(ctx, H.StateField(g, q), 0.0, 200 * dt, H.IntegratorConfig(fixed_dt=dt, h_floor=floor))
+    assert res.aborted
+    assert res.abort_reason == rec.reason.decode()
+    assert (res.accepted, res.rejected, res.rhs_evals) == (rec.accepted, rec.rejected, rec.rhs_evals)
+    assert res.t == rec.t
+    assert _neq(res.q.flat(), want) == 0
+
+
+def test_fused_launch_count_and_profile():
+    """2n+1 kernels per n-step graph chunk (S1, S2, (S31, S2)^(n-1), S3)."""
+    nx = ny = 256
+    og = omake_grid(nx, ny)
+    q, b = mms_exact_field(og, 0.3)
+    g, ctx = _ctx(og, b)
+    y = ctx.state(H.StateField(g, q))
+    k1 = ctx.state()
+    H.rhs(ctx, 0.0, y, k1)
+    done, ms, kernels = H.bs3_fixed_steps(ctx, y, k1, 0.0, 1e-5, 64)
+    assert done == 64 and kernels == 2 * 64 + 1
+    ctx.fused_stages = False
+    done, ms, kernels = H.bs3_fixed_steps(ctx, y, k1, 0.0, 1e-5, 64)
+    assert done == 64 and kernels == 3 * 64
