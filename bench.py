@@ -14,8 +14,9 @@ t = 0.3, lambda = 500, fixed dt = 0.25 dx / 20), plus achieved HBM GB/s.
 * ``e2e``     : the same metric through the public API with HOST buffers:
                 one ``adaptive_solve`` call (fixed dt, K steps) from a pinned
                 host state to a host result, H2D + D2H inside the timed region.
-* ``roofline``: the dominant kernel (stage 2), algorithmic bytes per launch
-                (168 B per node) / its mean launch time.
+* ``roofline``: the dominant kernel of the steady-state step (S2 or the
+                fused S3+S1 kernel S31, DESIGN.md sections 2b, 7), algorithmic
+                bytes per launch (168 / 128 B per node) / its mean launch time.
 * ``cpu_baseline``: the reference CPU path (oracle/_ref, or the C oracle port)
                 on this host's cores on a bounded sample.
 Multi-GPU (torchrun): weak scaling, every rank owns an 8192-row slab of a

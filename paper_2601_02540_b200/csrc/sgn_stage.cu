@@ -817,8 +817,12 @@ __device__ __forceinline__ void s31_half1(const StageArgs& A, const KPtrs& P, co
     for (int f = 0; f < 5; ++f) P.out2[f][off] = o[f];
 }
 
+#ifndef HSGN_S31_MINB
+#define HSGN_S31_MINB (16 / (BX / 32))  // 16 warps per SM (49 KB of rings per 128-thread CTA)
+#endif
+
 template <int KIND>
-__global__ void __launch_bounds__(BX, 4) sgn_s31_kernel(const StageArgs A, const KPtrs P) {
+__global__ void __launch_bounds__(BX, HSGN_S31_MINB) sgn_s31_kernel(const StageArgs A, const KPtrs P) {
     extern __shared__ __align__(16) double2 ring[];  // ring A | ring B, each 3 x NPF x BX
     __shared__ int s_skip;
     const int tid = threadIdx.x;

@@ -25,4 +25,7 @@ if len(sys.argv) > 4:
         done, ms, kern = H.bs3_fixed_steps(ctx, y, k1, 0.0, dt, steps)
         ms3 = (C.c_double * 3)()
         H.api.N.lib().hsgn_profile_stages(ctx._h, y._h, k1._h, dt, 3, ms3)
-        print(f"rep {rep}: ms/step={ms / max(done, 1):.3f} stages={[round(x, 3) for x in ms3]}")
+        m31 = C.c_double(0.0)
+        H.api.N.lib().hsgn_profile_fused(ctx._h, y._h, k1._h, dt, 3, C.byref(m31))
+        print(f"rep {rep}: ms/step={ms / max(done, 1):.3f} stages={[round(x, 3) for x in ms3]} "
+              f"S31={m31.value:.3f}")
