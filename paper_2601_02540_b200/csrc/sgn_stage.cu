@@ -760,17 +760,18 @@ struct Thr2 {
     unsigned long long bad_a, bad_b;
 };
 
-// S3 half at row r from ring-A slots (ap: row r-1, ac: row r, an: row r+1;
-// rh: 1/h of row r at this column): k4 (stored when owned) and the S1-half
-// input products of row r into ring-B slot bo (its 1/h into *rh_b).
+// S3 half at row r from ring-A slots (ap: row r-1, ac: row r; yn: the
+// y-quantities of row r+1 as products() just formed them, identical to the
+// ring re-form; rh: 1/h of row r at this column): k4 (stored when owned) and
+// the S1-half input products of row r into ring-B slot bo (their
+// y-quantities into yb, 1/h into *rh_b).
 template <int KIND>
 __device__ __forceinline__ void s31_half3(const StageArgs& A, const KPtrs& P, Thr2& T, const double2* ap,
-                                          const double2* ac, const double2* an, double rh, double2* bo,
+                                          const double2* ac, const YQ& yn, double rh, double2* bo, YQ& yb,
                                           double* rh_b, int r) {
     if (!T.fa) return;
-    YQ yp, yn;
+    YQ yp;
     neighbour_y(ap + T.tid, yp);
-    neighbour_y(an + T.tid, yn);
     const double cy = (r == T.jc0 || r == T.jc1) ? A.c1y : A.cpy;
     double o[5];
     tendency<KIND>(A, ac, T.tid, T.sl, T.sr, T.cx, cy, T.xl, T.xr, T.i, r, yp, yn, rh, o);
@@ -792,23 +793,24 @@ __device__ __forceinline__ void s31_half3(const StageArgs& A, const KPtrs& P, Th
     rb.b = p2.y;
 #pragma unroll
     for (int f = 0; f < 5; ++f) rb.k[f] = o[f];
-    YQ unused;
-    const bool ok = products<MODE_S1, false>(A, rb, bo + T.tid, unused, rh_b);
+    const bool ok = products<MODE_S1, false>(A, rb, bo + T.tid, yb, rh_b);
     if (own && !ok) ++T.bad_b;
 }
 
-// S1 half at row j from ring-B slots (bp: row j-1, bc: row j, bn: row j+1).
+// S1 half at row j from ring-B slots (bp: row j-1, bc: row j; ynb: the
+// y-quantities of row j+1 from the S3 half that just formed them).
 template <int KIND>
 __device__ __forceinline__ void s31_half1(const StageArgs& A, const KPtrs& P, const Thr2& T, const double2* bp,
-                                          const double2* bc, const double2* bn, double rh, int j) {
+                                          const double2* bc, const YQ& ynb, double rh, int j) {
     if (!T.fb) return;
     // a clamped (wall) row reads itself in place of the missing neighbour,
     // exactly the clamped stage input the unfused S1 forms there
     if (j == 0 && A.y_lo == YE_CLAMP) bp = bc;
-    if (j == A.ny - 1 && A.y_hi == YE_CLAMP) bn = bc;
-    YQ yp, yn;
+    YQ yp, yc;
     neighbour_y(bp + T.tid, yp);
-    neighbour_y(bn + T.tid, yn);
+    const bool hi = j == A.ny - 1 && A.y_hi == YE_CLAMP;
+    if (hi) neighbour_y(bc + T.tid, yc);
+    const YQ& yn = hi ? yc : ynb;
     const double cy = (j == T.jc0 || j == T.jc1) ? A.c1y : A.cpy;
     double o[5];
     tendency<KIND>(A, bc, T.tid, T.sl, T.sr, T.cx, cy, T.xl, T.xr, T.i, j, yp, yn, rh, o);
@@ -879,37 +881,37 @@ __global__ void __launch_bounds__(BX, HSGN_S31_MINB) sgn_s31_kernel(const StageA
     // row j0-1 (-> b0); row j0+1 -> a1; S3 half of row j0 (-> b1).  The
     // pointers then sit as iteration j0 expects.
     Raw raw;
-    YQ unused;
+    YQ ya, yb;  // y-quantities just formed for ring A / ring B (the next row of each half)
     double rh_m2, rh_m1, rh_0, rhb0;
     load_raw<MODE_S3>(P, (unsigned)map_row2(A, j0 - 2) * unx + T.col, raw);
-    products<MODE_S3, false>(A, raw, a1 + tid, unused, &rh_m2);
+    products<MODE_S3, false>(A, raw, a1 + tid, ya, &rh_m2);
     load_raw<MODE_S3>(P, (unsigned)map_row2(A, j0 - 1) * unx + T.col, raw);
-    products<MODE_S3, false>(A, raw, a2 + tid, unused, &rh_m1);
+    products<MODE_S3, false>(A, raw, a2 + tid, ya, &rh_m1);
     load_raw<MODE_S3>(P, (unsigned)map_row2(A, j0) * unx + T.col, raw);
-    if (!products<MODE_S3, false>(A, raw, a0 + tid, unused, &rh_0) && T.fb) ++T.bad_a;
+    if (!products<MODE_S3, false>(A, raw, a0 + tid, ya, &rh_0) && T.fb) ++T.bad_a;
     load_raw<MODE_S3>(P, (unsigned)map_row2(A, j0 + 1) * unx + T.col, raw);
     __syncthreads();
     // S3 half of row j0-1 (ring B row j0-1 -> b0)
-    s31_half3<KIND>(A, P, T, a1, a2, a0, rh_m1, b0, &rhb0, j0 - 1);
+    s31_half3<KIND>(A, P, T, a1, a2, ya, rh_m1, b0, yb, &rhb0, j0 - 1);
     // row j0+1 overwrites row j0-2's slot (a1): only this thread's own column
     // of row j0-2 was read (y-window of the S3 half above)
-    if (!products<MODE_S3, false>(A, raw, a1 + tid, unused, &rha1) && T.fb && j0 + 1 < T.j1) ++T.bad_a;
+    if (!products<MODE_S3, false>(A, raw, a1 + tid, ya, &rha1) && T.fb && j0 + 1 < T.j1) ++T.bad_a;
     load_raw<MODE_S3>(P, (unsigned)map_row2(A, j0 + 2) * unx + T.col, raw);
     // S3 half of row j0 (ring B row j0 -> b1)
-    s31_half3<KIND>(A, P, T, a2, a0, a1, rh_0, b1, &rhb1, j0);
+    s31_half3<KIND>(A, P, T, a2, a0, ya, rh_0, b1, yb, &rhb1, j0);
     __syncthreads();  // ring A row j0-1 (a2) is overwritten next; ring B rows j0-1, j0 published
 
 #pragma unroll 1
     for (int j = j0; j < T.j1; ++j) {
         // ynew row j+2 into the slot of row j-1 (a2), last read across
         // threads by the S3 half of row j-1 before the previous barrier
-        if (!products<MODE_S3, false>(A, raw, a2 + tid, unused, &rha2) && T.fb && j + 2 < T.j1) ++T.bad_a;
+        if (!products<MODE_S3, false>(A, raw, a2 + tid, ya, &rha2) && T.fb && j + 2 < T.j1) ++T.bad_a;
         if (j + 1 < T.j1) load_raw<MODE_S3>(P, (unsigned)map_row2(A, j + 3) * unx + T.col, raw);
         __syncthreads();
         // S3 half of row j+1 -> ring B row j+1 into the slot of row j-2 (b2),
         // last read across threads by the S1 half of row j-2
-        s31_half3<KIND>(A, P, T, a0, a1, a2, rha1, b2, &rhb2, j + 1);
-        s31_half1<KIND>(A, P, T, b0, b1, b2, rhb1, j);
+        s31_half3<KIND>(A, P, T, a0, a1, ya, rha1, b2, yb, &rhb2, j + 1);
+        s31_half1<KIND>(A, P, T, b0, b1, yb, rhb1, j);
         // rotate: A rows (j+1, j+2, j) -> (a0, a1, a2); B rows (j, j+1, j-1) -> (b0, b1, b2)
         double2* t = a0;
         a0 = a1;
