@@ -626,8 +626,8 @@ __global__ void __launch_bounds__(BX, min_blocks<MODE>()) sgn_stage_kernel(const
     T.cx = (T.xl || T.xr) ? A.c1x : A.cpx;
     T.sl = T.xl ? tid : tid - 1;
     T.sr = T.xr ? tid : tid + 1;
-    const int j0 = blockIdx.y * A.rows_per_block;
-    T.j1 = min(ny, j0 + A.rows_per_block);
+    const int j0 = A.band0 + blockIdx.y * A.rows_per_block;
+    T.j1 = min(A.band1 > 0 ? A.band1 : ny, j0 + A.rows_per_block);
     T.jc0 = A.y_lo == YE_CLAMP ? 0 : -2;
     T.jc1 = A.y_hi == YE_CLAMP ? ny - 1 : -2;
     T.bad = 0;
@@ -858,8 +858,8 @@ __global__ void __launch_bounds__(BX, HSGN_S31_MINB) sgn_s31_kernel(const StageA
     T.cx = (T.xl || T.xr) ? A.c1x : A.cpx;
     T.sl = T.xl ? tid : tid - 1;
     T.sr = T.xr ? tid : tid + 1;
-    T.j0 = blockIdx.y * A.rows_per_block;
-    T.j1 = min(ny, T.j0 + A.rows_per_block);
+    T.j0 = A.band0 + blockIdx.y * A.rows_per_block;
+    T.j1 = min(A.band1 > 0 ? A.band1 : ny, T.j0 + A.rows_per_block);
     T.jc0 = A.y_lo == YE_CLAMP ? 0 : INT_MIN;
     T.jc1 = A.y_hi == YE_CLAMP ? ny - 1 : INT_MIN;
     T.bad_a = 0;
@@ -958,6 +958,8 @@ __global__ void __launch_bounds__(256) sum_partials_kernel(const double* part, i
 
 __host__ __device__ constexpr size_t cmax(size_t a, size_t b) { return a < b ? b : a; }
 
+static int band_rows(const StageArgs& A) { return (A.band1 > 0 ? A.band1 : A.ny) - A.band0; }
+
 template <int MODE, bool TMA>
 __host__ __device__ constexpr size_t ring_bytes() {
     // (S2 must keep ~80 KB of L1 beside its rings -- 3 CTAs of 49 KB: its 16
@@ -976,7 +978,7 @@ static cudaError_t launch_tma(const StageArgs& A, const KPtrs& P, cudaStream_t s
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    dim3 grid((A.nx + WX - 1) / WX, (A.ny + A.rows_per_block - 1) / A.rows_per_block);
+    dim3 grid((A.nx + WX - 1) / WX, (band_rows(A) + A.rows_per_block - 1) / A.rows_per_block);
     sgn_stage_kernel<MODE, KIND, TMA><<<grid, BX, ring_bytes<MODE, TMA>(), st>>>(A, P);
     return cudaGetLastError();
 }
@@ -1020,7 +1022,7 @@ static cudaError_t launch_s31(const StageArgs& A, cudaStream_t st) {
         P.out2[f] = A.out2 + f * A.fs - g;
     }
     P.b = A.b - g;
-    dim3 grid((A.nx + WX2 - 1) / WX2, (A.ny + A.rows_per_block - 1) / A.rows_per_block);
+    dim3 grid((A.nx + WX2 - 1) / WX2, (band_rows(A) + A.rows_per_block - 1) / A.rows_per_block);
     sgn_s31_kernel<KIND><<<grid, BX, bytes, st>>>(A, P);
     return cudaGetLastError();
 }
