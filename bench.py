@@ -38,16 +38,18 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-BYTES_PER_NODE = {"S1": 128, "S2": 168, "S3": 88, "S31": 128}  # DESIGN.md sections 2b, 3
+BYTES_PER_NODE = {"S1": 128, "S2": 168, "S3": 88, "S31": 128, "STEP": 168}  # DESIGN.md sections 2b, 2c, 3
 
 
-def step_bytes_per_node(fused: bool, chunk: int = 64) -> float:
+def step_bytes_per_node(mode: int, chunk: int) -> float:
     """Algorithmic HBM bytes per node per step of the fixed-step pipeline:
-    unfused S1 + S2 + S3 = 384; fused chunks of n steps S1 + n S2 +
-    (n-1) S31 + S3 = 296 n + 88."""
-    if not fused:
+    mode 0 S1 + S2 + S3 = 384; mode 1 chunks of n steps S1 + n S2 +
+    (n-1) S31 + S3 = 296 n + 88; mode 2 one whole-step kernel = 168."""
+    if mode == 0:
         return 384.0
-    return (296.0 * chunk + 88.0) / chunk
+    if mode == 1:
+        return (296.0 * chunk + 88.0) / chunk
+    return 168.0
 METRIC = "grid-point RK-stage updates/sec on 8192² fp64 grid; achieved HBM GB/s"
 
 
@@ -191,7 +193,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--rows-per-block", type=int, default=0)
-    ap.add_argument("--unfused", action="store_true", help="one kernel per stage (A/B of the S31 fusion)")
+    ap.add_argument("--fusion", type=int, default=-1, choices=[-1, 0, 1, 2],
+                    help="fixed-step kernel structure (0 per stage, 1 S31, 2 whole step; -1 library default)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -221,9 +224,9 @@ def main():
         ctx = S.make_slab_context(g, phys, rank, world, local, dist)
     if args.rows_per_block:
         ctx.set_rows_per_block(args.rows_per_block)
-    if args.unfused:
-        ctx.fused_stages = False
-    fused = ctx.fused_stages and world == 1
+    if args.fusion >= 0:
+        ctx.fused_stages = args.fusion
+    mode = ctx.fused_stages if world == 1 else 0
     y = ctx.state(q)
     k1 = ctx.state()
     H.rhs(ctx, 0.0, y, k1)
@@ -249,13 +252,13 @@ def main():
     H.api._check(ctx, H.api.N.lib().hsgn_profile_stages(ctx._h, y._h, k1._h, dt, 3, ms3), "profile")
     ms3 = list(ms3)
     names = ["S1", "S2", "S3"]
-    if fused:  # the steady-state step is S2 + S31
-        m31 = H.api.N.D(0.0)
-        H.api._check(ctx, H.api.N.lib().hsgn_profile_fused(ctx._h, y._h, k1._h, dt, 3, H.api.C.byref(m31)),
+    if mode:  # the steady-state step is S2 + S31 (mode 1) or one STEP kernel (mode 2)
+        mf = H.api.N.D(0.0)
+        H.api._check(ctx, H.api.N.lib().hsgn_profile_fused(ctx._h, y._h, k1._h, dt, 3, H.api.C.byref(mf)),
                      "profile_fused")
-        ms3.append(m31.value)
-        names.append("S31")
-    cand = [1, 3] if fused else [0, 1, 2]
+        ms3.append(mf.value)
+        names.append("S31" if mode == 1 else "STEP")
+    cand = {0: [0, 1, 2], 1: [1, 3], 2: [3]}[mode]
     dom = max(cand, key=lambda k: ms3[k])
     peak, peak_kind = peaks()
     achieved = BYTES_PER_NODE[names[dom]] * points / (ms3[dom] * 1e-3) / 1e9
@@ -266,11 +269,13 @@ def main():
             traffic = json.load(fh).get(names[dom])
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic,
-                "kernel": "sgn_s31_kernel" if names[dom] == "S31" else f"sgn_stage_kernel<{names[dom]}>",
+                "kernel": {"S31": "sgn_s31_kernel", "STEP": "sgn_step_kernel"}.get(names[dom],
+                                                                                  f"sgn_stage_kernel<{names[dom]}>"),
+                "fixed_step_kernels": ["per stage", "S2 + S31", "whole step"][mode],
                 "bytes_per_node": BYTES_PER_NODE[names[dom]], "peak_source": peak_kind,
                 "stage_ms": {names[k]: ms3[k] for k in range(len(names))},
-                "step_bytes_per_node": step_bytes_per_node(fused),
-                "step_gbs": step_bytes_per_node(fused) * points / (ms / args.steps * 1e-3) / 1e9}
+                "step_bytes_per_node": step_bytes_per_node(mode, min(64, args.steps)),
+                "step_gbs": step_bytes_per_node(mode, min(64, args.steps)) * points / (ms / args.steps * 1e-3) / 1e9}
 
     # end-to-end through the public API with host buffers (pinned)
     e2e = None

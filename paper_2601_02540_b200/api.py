@@ -278,13 +278,14 @@ class RhsContext:
         _check(self, N.lib().hsgn_set_tma(self._h, int(bool(on))), "hsgn_set_tma")
 
     @property
-    def fused_stages(self) -> bool:
-        """Fixed-step graphs fuse stage 3 with the next step's stage 1."""
-        return bool(N.lib().hsgn_fused_stages(self._h))
+    def fused_stages(self) -> int:
+        """Fixed-step kernel structure: 0 per stage, 1 stage 3 fused with the
+        next stage 1 (S31), 2 one kernel per whole step."""
+        return int(N.lib().hsgn_fused_stages(self._h))
 
     @fused_stages.setter
-    def fused_stages(self, on: bool):
-        _check(self, N.lib().hsgn_set_fused_stages(self._h, int(bool(on))), "set_fused_stages")
+    def fused_stages(self, mode):
+        _check(self, N.lib().hsgn_set_fused_stages(self._h, int(mode)), "set_fused_stages")
 
     def state(self, host=None) -> DeviceState:
         return DeviceState(self, host)

@@ -130,7 +130,7 @@ struct hsgn_ctx {
     int forced_kind = -1;  // stencil kind override (tests); -1 = automatic
     int use_tma = 0;       // TMA staging of raw inputs when nx is even (opt-in: slower in r1)
     int in_group = 0;      // member of an in-process slab group (halo pulls by the group)
-    int fused = 1;         // fixed-step graphs use the S3+S1 kernel (whole-grid contexts)
+    int fused = 1;         // fixed-step graphs (whole-grid contexts): 0 per stage, 1 S31, 2 whole-step kernel
     int64_t n_evals = 0;
     std::string err;
     // workspace for the integrator
@@ -474,6 +474,53 @@ static hsgn_status enqueue_stage(hsgn_ctx* c, int stage, const hsgn_state* y, co
     return launch(c, MODE_S2, A);
 }
 
+// One whole fixed step (STEP kernel): y, k1 -> ynew, k4 with the records of
+// step `rec` (prev: the previous step's, for the halt test).
+static hsgn_status enqueue_step_kernel(hsgn_ctx* c, const hsgn_state* y, const hsgn_state* k1, hsgn_state* ynew,
+                                       hsgn_state* k4, StepRec* rec, const StepRec* prev, double dt) {
+    StageArgs A = stage_args(c, MODE_STEP, 0.0);
+    A.a = 0.5 * dt;
+    A.a2 = 0.75 * dt;
+    A.c1 = dt * (2.0 / 9.0);
+    A.c2 = dt * (1.0 / 3.0);
+    A.c3 = dt * (4.0 / 9.0);
+    A.y = y->base;
+    A.k = k1->base;
+    A.out = ynew->base;
+    A.out2 = k4->base;
+    A.bad = &rec->bad[0];
+    A.bad2 = &rec->bad[1];
+    A.bad3 = &rec->bad[2];
+    A.minh = &rec->minh;
+    A.halt = c->d_halt;
+    if (prev) {
+        A.chk_bad = &prev->bad[0];
+        A.chk_bad2 = &prev->bad[1];
+        A.chk_bad3 = &prev->bad[2];
+        A.chk_minh = &prev->minh;
+    }
+    return launch(c, MODE_STEP, A);
+}
+
+// A chunk of `steps` fixed steps, one STEP kernel each (+1 gauge gather per
+// step with a recorder).  Whole-grid contexts.
+static hsgn_status enqueue_chunk_step(hsgn_ctx* c, int parity, int steps, double dt, const hsgn_recorder* R) {
+    hsgn_state* Y[2] = {&c->ws[0], &c->ws[1]};
+    hsgn_state* K[2] = {&c->ws[2], &c->ws[3]};
+    const bool gauges = R && !R->gi.empty();
+    hsgn_status st;
+    for (int s = 0; s < steps; ++s) {
+        const int p = (parity + s) & 1;
+        if ((st = enqueue_step_kernel(c, Y[p], K[p], Y[p ^ 1], K[p ^ 1], &c->d_rec[s], s ? &c->d_rec[s - 1] : nullptr,
+                                      dt)))
+            return st;
+        if (gauges)
+            CK(launch_gauges(Y[p ^ 1]->base, c->b, R->d_idx, (int)R->gi.size(),
+                             R->d_gauge + (size_t)s * R->gi.size(), c->stream));
+    }
+    return HSGN_OK;
+}
+
 // A chunk of `steps` fixed steps from buffer parity `parity` with the fused
 // S3+S1 kernel between steps: S1, S2, (S31, S2) x (steps-1), S3 -- 2 steps+1
 // launches (+1 gauge gather per step with a recorder).  Whole-grid contexts.
@@ -768,9 +815,9 @@ hsgn_status hsgn_set_stencil_kind(hsgn_ctx* c, int32_t kind) {
 
 int32_t hsgn_stencil_kind(const hsgn_ctx* c) { return c ? c->base.pow2 : -1; }
 
-hsgn_status hsgn_set_fused_stages(hsgn_ctx* c, int32_t on) {
-    if (!c) return HSGN_EINVAL;
-    c->fused = on ? 1 : 0;
+hsgn_status hsgn_set_fused_stages(hsgn_ctx* c, int32_t mode) {
+    if (!c || mode < 0 || mode > 2) return HSGN_EINVAL;
+    c->fused = mode;
     return reconfigure(c);
 }
 
@@ -950,7 +997,8 @@ hsgn_status get_fixed_graph(hsgn_ctx* c, int steps, int parity, double dt, const
     CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
     reset_recs(c, steps);
     hsgn_status st = HSGN_OK;
-    if (c->fused && c->nranks == 1) st = enqueue_chunk_fused(c, parity, steps, dt, R, nullptr);
+    if (c->fused == 1 && c->nranks == 1) st = enqueue_chunk_fused(c, parity, steps, dt, R, nullptr);
+    if (c->fused == 2 && c->nranks == 1) st = enqueue_chunk_step(c, parity, steps, dt, R);
     for (int s = 0; s < steps && !st && !(c->fused && c->nranks == 1); ++s) {
         const int p = (parity + s) & 1;
         st = enqueue_step(c, Y[p], K[p], &c->ws[4], Y[p ^ 1], K[p ^ 1], nullptr, &c->d_rec[s],
@@ -993,7 +1041,7 @@ static hsgn_status run_fixed_chunk(hsgn_ctx* c, int parity, int steps, double t,
         FixedGraph* fg = nullptr;
         if ((st = get_fixed_graph(c, steps, parity, dt, R, &fg))) return st;
         CK(cudaGraphLaunch(fg->exec, c->stream));
-        if (kernels) *kernels += (gauges ? steps : 0) + (c->fused ? 2 * steps + 1 : 3 * steps);
+        if (kernels) *kernels += (gauges ? steps : 0) + (c->fused == 2 ? steps : c->fused ? 2 * steps + 1 : 3 * steps);
     } else {
         hsgn_state* Y[2] = {&c->ws[0], &c->ws[1]};
         hsgn_state* K[2] = {&c->ws[2], &c->ws[3]};
@@ -1646,9 +1694,12 @@ extern "C" hsgn_status hsgn_profile_fused(hsgn_ctx* c, const hsgn_state* y, cons
     double acc = 0.0;
     for (int r = 0; r < reps; ++r) {
         CK(cudaEventRecord(e0, c->stream));
-        if ((st = enqueue_stage(c, 31, &c->ws[0], &c->ws[2], &c->ws[4], &c->ws[1], &c->ws[3], nullptr,
-                                &c->d_rec[1], &c->d_rec[0], 0.0, dt, false, 0, 0)))
-            return st;
+        if (c->fused == 2)
+            st = enqueue_step_kernel(c, &c->ws[0], &c->ws[2], &c->ws[6], &c->ws[7], &c->d_rec[1], nullptr, dt);
+        else
+            st = enqueue_stage(c, 31, &c->ws[0], &c->ws[2], &c->ws[4], &c->ws[1], &c->ws[3], nullptr, &c->d_rec[1],
+                               &c->d_rec[0], 0.0, dt, false, 0, 0);
+        if (st) return st;
         CK(cudaEventRecord(e1, c->stream));
         CK(cudaEventSynchronize(e1));
         float m = 0.f;

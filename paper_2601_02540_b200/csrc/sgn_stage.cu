@@ -103,17 +103,12 @@ __device__ __forceinline__ void load_raw(const KPtrs& P, unsigned off, Raw& r) {
     r.b = __ldg(P.b + off);
 }
 
-// Pointwise products of rhs.hpp:99-109 at one node, from the stage input
-// q = y + a*k (state_add1, time_integration.hpp:61-75).  Stores the ring
-// pairs of the node (S already offset by ring row and column), fills the
-// y-quantities; returns h > 0.
-template <int MODE, bool STORE_RH = true>
-__device__ __forceinline__ bool products(const StageArgs& A, const Raw& raw, double2* S, YQ& Y, double* rh_out = nullptr) {
-    double q[5];
-#pragma unroll
-    for (int f = 0; f < 5; ++f)
-        q[f] = (MODE == MODE_S1 || MODE == MODE_S2) ? dadd(raw.y[f], dmul(A.a, raw.k[f])) : raw.y[f];
-    const double h = q[0], u = q[1], v = q[2], w = q[3], e = q[4], b = raw.b;
+// Pointwise products of rhs.hpp:99-109 at one node from the stage input q
+// (h, u, v, w, eta) and b: stores the ring pairs of the node (S already
+// offset by ring row and column), fills the y-quantities; returns h > 0.
+template <bool STORE_RH = true>
+__device__ __forceinline__ bool products_q(const double q[5], double b, double2* S, YQ& Y, double* rh_out) {
+    const double h = q[0], u = q[1], v = q[2], w = q[3], e = q[4];
     const bool ok = h > 0.0;
     const double rh = __drcp_rn(h);
     bool slow = false;
@@ -127,14 +122,6 @@ __device__ __forceinline__ bool products(const StageArgs& A, const Raw& raw, dou
     S[P_RHB * BX] = make_double2(r, hpb);
     if (STORE_RH) S[P_RH * BX] = make_double2(rh, 0.0);
     if (rh_out) *rh_out = rh;
-    if (MODE == MODE_S2) {  // ((y + c1 k1) + c2 k2): the k3-free part of ynew (state_add3)
-        double yp[5];
-#pragma unroll
-        for (int f = 0; f < 5; ++f) yp[f] = dadd(dadd(raw.y[f], dmul(A.c1, raw.kc[f])), dmul(A.c2, raw.k[f]));
-        S[P_YP01 * BX] = make_double2(yp[0], yp[1]);
-        S[P_YP23 * BX] = make_double2(yp[2], yp[3]);
-        S[P_YP4 * BX] = make_double2(yp[4], 0.0);
-    }
     Y.h = h;
     Y.u = u;
     Y.v = v;
@@ -147,6 +134,27 @@ __device__ __forceinline__ bool products(const StageArgs& A, const Raw& raw, dou
     Y.huv = dmul(dmul(h, u), v);  // (h*u)*v
     Y.e2h = dmul(e, r);
     Y.hvw = dmul(hv, w);
+    return ok;
+}
+
+// The same from raw stage data: q = y + a*k (state_add1,
+// time_integration.hpp:61-75) for S1/S2, q = y otherwise; S2 also stores
+// ((y + c1 k1) + c2 k2), the k3-free part of ynew (state_add3).
+template <int MODE, bool STORE_RH = true>
+__device__ __forceinline__ bool products(const StageArgs& A, const Raw& raw, double2* S, YQ& Y, double* rh_out = nullptr) {
+    double q[5];
+#pragma unroll
+    for (int f = 0; f < 5; ++f)
+        q[f] = (MODE == MODE_S1 || MODE == MODE_S2) ? dadd(raw.y[f], dmul(A.a, raw.k[f])) : raw.y[f];
+    const bool ok = products_q<STORE_RH>(q, raw.b, S, Y, rh_out);
+    if (MODE == MODE_S2) {
+        double yp[5];
+#pragma unroll
+        for (int f = 0; f < 5; ++f) yp[f] = dadd(dadd(raw.y[f], dmul(A.c1, raw.kc[f])), dmul(A.c2, raw.k[f]));
+        S[P_YP01 * BX] = make_double2(yp[0], yp[1]);
+        S[P_YP23 * BX] = make_double2(yp[2], yp[3]);
+        S[P_YP4 * BX] = make_double2(yp[4], 0.0);
+    }
     return ok;
 }
 
@@ -928,6 +936,205 @@ __global__ void __launch_bounds__(BX, HSGN_S31_MINB) sgn_s31_kernel(const StageA
     if (T.bad_b) atomicAdd(A.bad2, T.bad_b);
 }
 
+// ------------------------------------------------------------ whole step
+// One fixed BS3 step in one pass (whole-grid contexts): reads y, k1 (= f(y),
+// FSAL) and b, writes ynew and k4 = f(ynew): 168 B/node per step.  The three
+// stages run as a pipeline inside the CTA, each one row (and one column)
+// behind the previous one:
+//   iteration r:  P1  stage-1 input y + a1 k1 of row r      -> ring R1
+//                 ---- barrier ----
+//                 F1  k2 at row r-1; stage-2 input y + a2 k2 -> ring R2
+//                     and ((y + c1 k1) + c2 k2) kept in registers
+//                 F2  k3 at row r-2; ynew = part + c3 k3 (stored, min h)
+//                                                          -> ring R3
+//                 F3  k4 at row r-3 (stored)
+// Tiles: thread t holds column i0-3+t; F1 finishes threads 1..BX-2, F2
+// 2..BX-3, F3 3..BX-4 (WX3 = BX-6 columns per CTA).  Rows: the CTA owns
+// [j0, j1); F3 runs those rows, F2 one more above and below, F1 two, P1
+// three.  Every operation is the unfused stages' (bit-identical); the rings
+// are the S31 layout (4 pairs, 1/h in registers), 72 KB per CTA.
+constexpr int WX3 = BX - 6;
+
+#ifndef HSGN_STEP_MINB
+#define HSGN_STEP_MINB (12 / (BX / 32))  // 12 warps per SM (3 x 72 KB of rings)
+#endif
+
+// y-quantities of the row above / below at this column for a finish at row
+// j: the ring entry of the neighbour row, or (clamped wall rows) the row's
+// own entry, as the unfused kernels' clamped stage input gives.
+__device__ __forceinline__ void ywin_prev(const StageArgs& A, int j, const double2* prev, const double2* cur, int tid,
+                                          YQ& Y) {
+    neighbour_y((j == 0 && A.y_lo == YE_CLAMP ? cur : prev) + tid, Y);
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(BX, HSGN_STEP_MINB) sgn_step_kernel(const StageArgs A, const KPtrs P) {
+    extern __shared__ __align__(16) double2 ring[];  // R1 | R2 | R3, each 3 x NPF x BX
+    __shared__ unsigned long long s_min[BX / 32];
+    __shared__ int s_skip;
+    const int tid = threadIdx.x;
+    if (A.halt) {  // failure protocol: the previous step's record
+        if (tid == 0) {
+            int skip = *A.halt;
+            if (!skip && A.chk_bad && *A.chk_bad) skip = 1;
+            if (!skip && A.chk_bad2 && *A.chk_bad2) skip = 1;
+            if (!skip && A.chk_bad3 && *A.chk_bad3) skip = 1;
+            if (!skip && A.chk_minh) {
+                const unsigned long long mb = *A.chk_minh;
+                if (mb != ~0ull && __longlong_as_double((long long)mb) <= A.h_floor) skip = 1;
+            }
+            if (skip) *A.halt = 1;
+            s_skip = skip;
+        }
+        __syncthreads();
+        if (s_skip) return;
+    }
+    const int nx = A.nx, ny = A.ny;
+    const int i = (int)blockIdx.x * WX3 - 3 + tid;
+    const bool f1 = tid >= 1 && tid <= BX - 2 && i >= -2 && i <= nx + 1;
+    const bool f2 = tid >= 2 && tid <= BX - 3 && i >= -1 && i <= nx;
+    const bool f3 = tid >= 3 && tid <= BX - 4 && i >= 0 && i < nx;
+    int c = i;
+    if (i < 0) c = A.x_bounded ? 0 : nx + i;
+    if (i >= nx) c = (A.x_bounded || i > nx + 2) ? nx - 1 : i - nx;
+    const unsigned col = (unsigned)c;
+    const bool xl = A.x_bounded && i == 0, xr = A.x_bounded && i == nx - 1;
+    const double cx = (xl || xr) ? A.c1x : A.cpx;
+    const int sl = xl ? tid : tid - 1, sr = xr ? tid : tid + 1;
+    const int j0 = A.band0 + blockIdx.y * A.rows_per_block;
+    const int j1 = min(A.band1 > 0 ? A.band1 : ny, j0 + A.rows_per_block);
+    const int jc0 = A.y_lo == YE_CLAMP ? 0 : INT_MIN, jc1 = A.y_hi == YE_CLAMP ? ny - 1 : INT_MIN;
+    const bool clamp_hi = A.y_hi == YE_CLAMP;
+    const unsigned unx = (unsigned)nx;
+    unsigned long long bad1 = 0, bad2 = 0, bad3 = 0, my_min = ~0ull;
+
+    constexpr int SLOT = NPF * BX;
+    // rotating slots: at iteration r, ring k holds rows (c-2, c-1, c) in
+    // (pa, pb, pc) where c = r, r-1, r-2 for R1, R2, R3 (pc is written now)
+    double2 *p1a = ring, *p1b = ring + SLOT, *p1c = ring + 2 * SLOT;
+    double2 *p2a = ring + 3 * SLOT, *p2b = ring + 4 * SLOT, *p2c = ring + 5 * SLOT;
+    double2 *p3a = ring + 6 * SLOT, *p3b = ring + 7 * SLOT, *p3c = ring + 8 * SLOT;
+    double rh1p = 0.0, rh2p = 0.0, rh3p = 0.0;  // 1/h of R1 row r-1, R2 row r-2, R3 row r-3
+    double partp[5];                            // ((y + c1 k1) + c2 k2) of row r-2
+#pragma unroll
+    for (int f = 0; f < 5; ++f) partp[f] = 0.0;
+
+    Raw raw;
+    load_raw<MODE_S1>(P, (unsigned)map_row2(A, j0 - 3) * unx + col, raw);
+#pragma unroll 1
+    for (int r = j0 - 3; r <= j1 + 2; ++r) {
+        // ---- P1: stage-1 input of row r; raw of row r+1 is loaded right away
+        // (in flight across the three finishes)
+        double rh1c;
+        {
+            YQ unused;
+            const bool ok = products<MODE_S1, false>(A, raw, p1c + tid, unused, &rh1c);
+            if (f3 && r >= j0 && r < j1 && !ok) ++bad1;
+        }
+        if (r + 1 <= j1 + 2) load_raw<MODE_S1>(P, (unsigned)map_row2(A, r + 1) * unx + col, raw);
+        __syncthreads();
+        // ---- F1: k2 at row r-1 -> stage-2 input -> R2 (slot p2c)
+        double rh2c = 0.0, partc[5];
+        if (r - 1 >= j0 - 2 && f1) {
+            const int j = r - 1;
+            // y, k1 of row j again (this thread loaded them one row ago: L1/L2)
+            const unsigned offj = (unsigned)map_row2(A, j) * unx + col;
+            double yj[5], kj[5];
+#pragma unroll
+            for (int f = 0; f < 5; ++f) {
+                yj[f] = __ldg(P.y[f] + offj);
+                kj[f] = __ldg(P.k[f] + offj);
+            }
+            YQ yp, yn;
+            ywin_prev(A, j, p1a, p1b, tid, yp);
+            neighbour_y((clamp_hi && j == ny - 1 ? p1b : p1c) + tid, yn);
+            const double cy = (j == jc0 || j == jc1) ? A.c1y : A.cpy;
+            double k2[5];
+            tendency<KIND>(A, p1b, tid, sl, sr, cx, cy, xl, xr, i, j, yp, yn, rh1p, k2);
+            double q[5];
+#pragma unroll
+            for (int f = 0; f < 5; ++f) {
+                q[f] = dadd(yj[f], dmul(A.a2, k2[f]));
+                partc[f] = dadd(dadd(yj[f], dmul(A.c1, kj[f])), dmul(A.c2, k2[f]));
+            }
+            YQ unused;
+            const bool ok = products_q<false>(q, p1b[tid + P_EB * BX].y, p2c + tid, unused, &rh2c);
+            if (f3 && j >= j0 && j < j1 && !ok) ++bad2;
+        }
+        // ---- F2: k3 at row r-2 -> ynew (stored) -> R3 (slot p3c)
+        YQ y3;
+        double rh3c = 0.0;
+        if (r - 2 >= j0 - 1 && f2) {
+            const int j = r - 2;
+            YQ yp, yn;
+            ywin_prev(A, j, p2a, p2b, tid, yp);
+            neighbour_y((clamp_hi && j == ny - 1 ? p2b : p2c) + tid, yn);
+            const double cy = (j == jc0 || j == jc1) ? A.c1y : A.cpy;
+            double k3[5];
+            tendency<KIND>(A, p2b, tid, sl, sr, cx, cy, xl, xr, i, j, yp, yn, rh2p, k3);
+            double ynw[5];
+#pragma unroll
+            for (int f = 0; f < 5; ++f) ynw[f] = dadd(partp[f], dmul(A.c3, k3[f]));  // state_add3
+            const bool own = f3 && j >= j0 && j < j1;
+            if (own) {
+                const unsigned off = (unsigned)(j + 1) * unx + col;
+#pragma unroll
+                for (int f = 0; f < 5; ++f) P.out[f][off] = ynw[f];
+                const unsigned long long bits = (unsigned long long)__double_as_longlong(ynw[0]);
+                my_min = bits < my_min ? bits : my_min;
+            }
+            const bool ok = products_q<false>(ynw, p2b[tid + P_EB * BX].y, p3c + tid, y3, &rh3c);
+            if (own && !ok) ++bad3;
+        }
+        // ---- F3: k4 at row r-3 (stored)
+        if (r - 3 >= j0 && f3) {
+            const int j = r - 3;
+            YQ yp;
+            ywin_prev(A, j, p3a, p3b, tid, yp);
+            YQ yc;
+            const bool hi = clamp_hi && j == ny - 1;
+            if (hi) neighbour_y(p3b + tid, yc);
+            const double cy = (j == jc0 || j == jc1) ? A.c1y : A.cpy;
+            double k4[5];
+            tendency<KIND>(A, p3b, tid, sl, sr, cx, cy, xl, xr, i, j, yp, hi ? yc : y3, rh3p, k4);
+            const unsigned off = (unsigned)(j + 1) * unx + col;
+#pragma unroll
+            for (int f = 0; f < 5; ++f) P.out2[f][off] = k4[f];
+        }
+        // ---- rotate
+        double2* t = p1a;
+        p1a = p1b;
+        p1b = p1c;
+        p1c = t;
+        t = p2a;
+        p2a = p2b;
+        p2b = p2c;
+        p2c = t;
+        t = p3a;
+        p3a = p3b;
+        p3b = p3c;
+        p3c = t;
+        rh1p = rh1c;
+        rh2p = rh2c;
+        rh3p = rh3c;
+#pragma unroll
+        for (int f = 0; f < 5; ++f) partp[f] = partc[f];
+    }
+    if (bad1) atomicAdd(A.bad, bad1);
+    if (bad2) atomicAdd(A.bad2, bad2);
+    if (bad3) atomicAdd(A.bad3, bad3);
+    if (A.minh) {
+        const unsigned long long m = warp_min_u64(my_min);
+        if ((tid & 31) == 0) s_min[tid >> 5] = m;
+        __syncthreads();
+        if (tid == 0) {
+            unsigned long long mm = s_min[0];
+            for (int k = 1; k < BX / 32; ++k) mm = s_min[k] < mm ? s_min[k] : mm;
+            if (mm != ~0ull) atomicMin(A.minh, mm);
+        }
+    }
+}
+
 // Deterministic final sum of per-block partials (single CTA, fixed order,
 // compensated); result goes to out[0].
 __global__ void __launch_bounds__(256) sum_partials_kernel(const double* part, int n, double* out) {
@@ -1028,8 +1235,35 @@ static cudaError_t launch_s31(const StageArgs& A, cudaStream_t st) {
 }
 
 template <int KIND>
+static cudaError_t launch_step(const StageArgs& A, cudaStream_t st) {
+    constexpr size_t bytes = sizeof(double2) * 3 * 3 * NPF * BX;
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e =
+            cudaFuncSetAttribute(sgn_step_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    KPtrs P;
+    const long long g = A.nx;
+    for (int f = 0; f < 5; ++f) {
+        P.y[f] = A.y + f * A.fs - g;
+        P.k[f] = A.k + f * A.fs - g;
+        P.kc[f] = P.yold[f] = nullptr;
+        P.part[f] = nullptr;
+        P.out[f] = A.out + f * A.fs - g;
+        P.out2[f] = A.out2 + f * A.fs - g;
+    }
+    P.b = A.b - g;
+    dim3 grid((A.nx + WX3 - 1) / WX3, (band_rows(A) + A.rows_per_block - 1) / A.rows_per_block);
+    sgn_step_kernel<KIND><<<grid, BX, bytes, st>>>(A, P);
+    return cudaGetLastError();
+}
+
+template <int KIND>
 static cudaError_t launch_kind(int mode, const StageArgs& A, cudaStream_t st) {
     switch (mode) {
+        case MODE_STEP: return launch_step<KIND>(A, st);
         case MODE_S31: return launch_s31<KIND>(A, st);
         case MODE_RHS: return launch_mode<MODE_RHS, KIND>(A, st);
         case MODE_S1: return launch_mode<MODE_S1, KIND>(A, st);

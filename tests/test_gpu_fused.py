@@ -48,13 +48,12 @@ def test_fused_fixed_steps_bitwise(orc, nx, ny, kx, ky, rpb):
     g, ctx = _ctx(og, b)
     if rpb:
         ctx.set_rows_per_block(rpb)
-    assert ctx.fused_stages
-    res = H.adaptive_solve(ctx, H.StateField(g, q), 0.0, T, H.IntegratorConfig(fixed_dt=dt))
-    assert (res.accepted, res.rhs_evals, res.aborted) == (rec.accepted, rec.rhs_evals, bool(rec.aborted))
-    assert _neq(res.q.flat(), want) == 0
-    ctx.fused_stages = False
-    res2 = H.adaptive_solve(ctx, H.StateField(g, q), 0.0, T, H.IntegratorConfig(fixed_dt=dt))
-    assert _neq(res2.q.flat(), want) == 0
+    for mode in (0, 1, 2):
+        ctx.fused_stages = mode
+        assert ctx.fused_stages == mode
+        res = H.adaptive_solve(ctx, H.StateField(g, q), 0.0, T, H.IntegratorConfig(fixed_dt=dt))
+        assert (res.accepted, res.rhs_evals, res.aborted) == (rec.accepted, rec.rhs_evals, bool(rec.aborted))
+        assert _neq(res.q.flat(), want) == 0, f"mode {mode}"
 
 
 def _drying_state(nx, ny, amp, U):
@@ -71,7 +70,7 @@ def _drying_state(nx, ny, amp, U):
 @pytest.mark.parametrize("amp,U,dt,floor", [(0.99, 10.0, 1e-3, 1e-12), (0.99, 30.0, 1e-3, 1e-12),
                                              (0.99, 10.0, 1e-3, 0.005), (0.999, 10.0, 1e-3, 0.005),
                                              (0.99, 10.0, 3e-3, 1e-12)])
-@pytest.mark.parametrize("fused", [True, False])
+@pytest.mark.parametrize("fused", [0, 1, 2])
 def test_fixed_step_failures_match_reference(orc, amp, U, dt, floor, fused):
     nx, ny = 64, 48
     og = omake_grid(nx, ny)
@@ -91,7 +90,8 @@ def test_fixed_step_failures_match_reference(orc, amp, U, dt, floor, fused):
 
 
 def test_fused_launch_count_and_profile():
-    """2n+1 kernels per n-step graph chunk (S1, S2, (S31, S2)^(n-1), S3)."""
+    """Kernels per n-step graph chunk: 3n per stage, 2n+1 with S31 (S1, S2,
+    (S31, S2)^(n-1), S3), n with the whole-step kernel."""
     nx = ny = 256
     og = omake_grid(nx, ny)
     q, b = mms_exact_field(og, 0.3)
@@ -99,8 +99,7 @@ def test_fused_launch_count_and_profile():
     y = ctx.state(H.StateField(g, q))
     k1 = ctx.state()
     H.rhs(ctx, 0.0, y, k1)
-    done, ms, kernels = H.bs3_fixed_steps(ctx, y, k1, 0.0, 1e-5, 64)
-    assert done == 64 and kernels == 2 * 64 + 1
-    ctx.fused_stages = False
-    done, ms, kernels = H.bs3_fixed_steps(ctx, y, k1, 0.0, 1e-5, 64)
-    assert done == 64 and kernels == 3 * 64
+    for mode, want in ((1, 2 * 64 + 1), (0, 3 * 64), (2, 64)):
+        ctx.fused_stages = mode
+        done, ms, kernels = H.bs3_fixed_steps(ctx, y, k1, 0.0, 1e-5, 64)
+        assert done == 64 and kernels == want, mode
