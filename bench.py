@@ -38,18 +38,24 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-BYTES_PER_NODE = {"S1": 128, "S2": 168, "S3": 88, "S31": 128, "STEP": 168}  # DESIGN.md sections 2b, 2c, 3
+BYTES_PER_NODE = {"S1": 128, "S2": 168, "S3": 88, "S31": 128, "STEP": 168, "S12": 128}
+# FP64 instructions (DADD + DMUL + DFMA) per node of each kernel, from the ncu
+# SASS mixes in profiles/ (r1_sass_mix_stage_kernels.txt, r1f_sass_mix_s31.txt,
+# r1g_sass_mix_s12.txt): the compute roofline of the FP64-issue-bound kernels
+FP64_PER_NODE = {"S1": 199.5, "S2": 228.8, "S3": 189.1, "S31": 397.3, "S12": 439.6}
+FP64_LANES_PER_SM, N_SM = 64, 148
 
 
 def step_bytes_per_node(mode: int, chunk: int) -> float:
     """Algorithmic HBM bytes per node per step of the fixed-step pipeline:
     mode 0 S1 + S2 + S3 = 384; mode 1 chunks of n steps S1 + n S2 +
-    (n-1) S31 + S3 = 296 n + 88; mode 2 one whole-step kernel = 168."""
+    (n-1) S31 + S3 = 296 n + 88; mode 2 one whole-step kernel = 168;
+    mode 3 S12 + S3 = 128 + 88 = 216."""
     if mode == 0:
         return 384.0
     if mode == 1:
         return (296.0 * chunk + 88.0) / chunk
-    return 168.0
+    return 168.0 if mode == 2 else 216.0
 METRIC = "grid-point RK-stage updates/sec on 8192² fp64 grid; achieved HBM GB/s"
 
 
@@ -193,8 +199,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--rows-per-block", type=int, default=0)
-    ap.add_argument("--fusion", type=int, default=-1, choices=[-1, 0, 1, 2],
-                    help="fixed-step kernel structure (0 per stage, 1 S31, 2 whole step; -1 library default)")
+    ap.add_argument("--fusion", type=int, default=-1, choices=[-1, 0, 1, 2, 3],
+                    help="fixed-step kernel structure (0 per stage, 1 S31, 2 whole step, 3 S12 + S3; "
+                         "-1 library default)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -252,13 +259,13 @@ def main():
     H.api._check(ctx, H.api.N.lib().hsgn_profile_stages(ctx._h, y._h, k1._h, dt, 3, ms3), "profile")
     ms3 = list(ms3)
     names = ["S1", "S2", "S3"]
-    if mode:  # the steady-state step is S2 + S31 (mode 1) or one STEP kernel (mode 2)
+    if mode:  # steady-state step: S2 + S31 (mode 1), STEP (mode 2), S12 + S3 (mode 3)
         mf = H.api.N.D(0.0)
         H.api._check(ctx, H.api.N.lib().hsgn_profile_fused(ctx._h, y._h, k1._h, dt, 3, H.api.C.byref(mf)),
                      "profile_fused")
         ms3.append(mf.value)
-        names.append("S31" if mode == 1 else "STEP")
-    cand = {0: [0, 1, 2], 1: [1, 3], 2: [3]}[mode]
+        names.append({1: "S31", 2: "STEP", 3: "S12"}[mode])
+    cand = {0: [0, 1, 2], 1: [1, 3], 2: [3], 3: [2, 3]}[mode]
     dom = max(cand, key=lambda k: ms3[k])
     peak, peak_kind = peaks()
     achieved = BYTES_PER_NODE[names[dom]] * points / (ms3[dom] * 1e-3) / 1e9
@@ -267,11 +274,19 @@ def main():
     if os.path.exists(tpath):
         with open(tpath) as fh:
             traffic = json.load(fh).get(names[dom])
+    fp64 = None
+    if names[dom] in FP64_PER_NODE:
+        sm_mhz = clk.summary().get("sm_mhz") or 1965.0
+        got = FP64_PER_NODE[names[dom]] * points / (ms3[dom] * 1e-3) / 1e9
+        top = FP64_LANES_PER_SM * N_SM * sm_mhz * 1e-3
+        fp64 = {"unit": "G FP64 thread-instr/s", "instr_per_node": FP64_PER_NODE[names[dom]], "achieved": got,
+                "peak": top, "frac": got / top, "peak_basis": f"{FP64_LANES_PER_SM} lanes x {N_SM} SMs x sm_mhz"}
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "fp64": fp64,
                 "traffic": traffic,
-                "kernel": {"S31": "sgn_s31_kernel", "STEP": "sgn_step_kernel"}.get(names[dom],
-                                                                                  f"sgn_stage_kernel<{names[dom]}>"),
-                "fixed_step_kernels": ["per stage", "S2 + S31", "whole step"][mode],
+                "kernel": {"S31": "sgn_s31_kernel", "STEP": "sgn_step_kernel", "S12": "sgn_s12_kernel"}.get(
+                    names[dom], f"sgn_stage_kernel<{names[dom]}>"),
+                "fixed_step_kernels": ["per stage", "S2 + S31", "whole step", "S12 + S3"][mode],
                 "bytes_per_node": BYTES_PER_NODE[names[dom]], "peak_source": peak_kind,
                 "stage_ms": {names[k]: ms3[k] for k in range(len(names))},
                 "step_bytes_per_node": step_bytes_per_node(mode, min(64, args.steps)),

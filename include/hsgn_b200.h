@@ -125,9 +125,10 @@ hsgn_status hsgn_set_tma(hsgn_ctx* ctx, int32_t on);
 int32_t hsgn_tma_enabled(const hsgn_ctx* ctx);
 
 /* Kernel structure of the fixed-step graphs of a whole-grid context (all
- * bit-identical, DESIGN.md sections 2b, 2c): 0 = one kernel per stage,
+ * bit-identical): 0 = one kernel per stage,
  * 1 = stage 3 of step n fused with stage 1 of step n+1 (S31), 2 = one
- * kernel per whole step.  Slab contexts always run one kernel per stage. */
+ * kernel per whole step, 3 (default) = stages 1+2 fused (S12), then stage 3.
+ * Slab contexts always run one kernel per stage. */
 hsgn_status hsgn_set_fused_stages(hsgn_ctx* ctx, int32_t mode);
 int32_t hsgn_fused_stages(const hsgn_ctx* ctx);
 
@@ -230,8 +231,8 @@ double hsgn_outer_sum(const hsgn_grid* grid, const double* rows, int32_t j_begin
 hsgn_status hsgn_profile_stages(hsgn_ctx* ctx, const hsgn_state* y, const hsgn_state* k1, double dt,
                                 int32_t reps, double* ms3);
 
-/* Mean device ms of the fused kernel of the current mode (S31, or the
- * whole-step kernel in mode 2) over `reps` launches. */
+/* Mean device ms of the fused kernel of the current mode (S31 in mode 1,
+ * the whole-step kernel in mode 2, S12 in mode 3) over `reps` launches. */
 hsgn_status hsgn_profile_fused(hsgn_ctx* ctx, const hsgn_state* y, const hsgn_state* k1, double dt, int32_t reps,
                                double* ms);
 

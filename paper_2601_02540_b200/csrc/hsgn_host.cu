@@ -130,7 +130,7 @@ struct hsgn_ctx {
     int forced_kind = -1;  // stencil kind override (tests); -1 = automatic
     int use_tma = 0;       // TMA staging of raw inputs when nx is even (opt-in: slower in r1)
     int in_group = 0;      // member of an in-process slab group (halo pulls by the group)
-    int fused = 1;         // fixed-step graphs (whole-grid contexts): 0 per stage, 1 S31, 2 whole-step kernel
+    int fused = 3;         // fixed-step graphs (whole-grid contexts): 0 per stage, 1 S31, 2 whole step, 3 S12 + S3
     int64_t n_evals = 0;
     std::string err;
     // workspace for the integrator
@@ -521,6 +521,47 @@ static hsgn_status enqueue_chunk_step(hsgn_ctx* c, int parity, int steps, double
     return HSGN_OK;
 }
 
+// A chunk of `steps` fixed steps as S12 (stages 1+2) + S3 per step.
+static hsgn_status enqueue_chunk_s12(hsgn_ctx* c, int parity, int steps, double dt, const hsgn_recorder* R) {
+    hsgn_state* Y[2] = {&c->ws[0], &c->ws[1]};
+    hsgn_state* K[2] = {&c->ws[2], &c->ws[3]};
+    const bool gauges = R && !R->gi.empty();
+    hsgn_status st;
+    for (int s = 0; s < steps; ++s) {
+        const int p = (parity + s) & 1;
+        StepRec* rec = &c->d_rec[s];
+        const StepRec* prev = s ? &c->d_rec[s - 1] : nullptr;
+        StageArgs A = stage_args(c, MODE_S12, 0.0);
+        A.a = 0.5 * dt;
+        A.a2 = 0.75 * dt;
+        A.c1 = dt * (2.0 / 9.0);
+        A.c2 = dt * (1.0 / 3.0);
+        A.c3 = dt * (4.0 / 9.0);
+        A.y = Y[p]->base;
+        A.k = K[p]->base;
+        A.out = Y[p ^ 1]->base;
+        A.bad = &rec->bad[0];
+        A.bad2 = &rec->bad[1];
+        A.minh = &rec->minh;
+        A.halt = c->d_halt;
+        A.chk_bad = prev ? &prev->bad[2] : nullptr;
+        A.chk_minh = prev ? &prev->minh : nullptr;
+        if ((st = launch(c, MODE_S12, A))) return st;
+        if (gauges)
+            CK(launch_gauges(Y[p ^ 1]->base, c->b, R->d_idx, (int)R->gi.size(),
+                             R->d_gauge + (size_t)s * R->gi.size(), c->stream));
+        A = stage_args(c, MODE_S3, dt);  // k4 = f(ynew), FSAL
+        A.y = Y[p ^ 1]->base;
+        A.out = K[p ^ 1]->base;
+        A.bad = &rec->bad[2];
+        A.halt = c->d_halt;
+        A.chk_bad = &rec->bad[1];
+        A.chk_bad2 = &rec->bad[0];
+        if ((st = launch(c, MODE_S3, A))) return st;
+    }
+    return HSGN_OK;
+}
+
 // A chunk of `steps` fixed steps from buffer parity `parity` with the fused
 // S3+S1 kernel between steps: S1, S2, (S31, S2) x (steps-1), S3 -- 2 steps+1
 // launches (+1 gauge gather per step with a recorder).  Whole-grid contexts.
@@ -816,7 +857,7 @@ hsgn_status hsgn_set_stencil_kind(hsgn_ctx* c, int32_t kind) {
 int32_t hsgn_stencil_kind(const hsgn_ctx* c) { return c ? c->base.pow2 : -1; }
 
 hsgn_status hsgn_set_fused_stages(hsgn_ctx* c, int32_t mode) {
-    if (!c || mode < 0 || mode > 2) return HSGN_EINVAL;
+    if (!c || mode < 0 || mode > 3) return HSGN_EINVAL;
     c->fused = mode;
     return reconfigure(c);
 }
@@ -999,6 +1040,7 @@ hsgn_status get_fixed_graph(hsgn_ctx* c, int steps, int parity, double dt, const
     hsgn_status st = HSGN_OK;
     if (c->fused == 1 && c->nranks == 1) st = enqueue_chunk_fused(c, parity, steps, dt, R, nullptr);
     if (c->fused == 2 && c->nranks == 1) st = enqueue_chunk_step(c, parity, steps, dt, R);
+    if (c->fused == 3 && c->nranks == 1) st = enqueue_chunk_s12(c, parity, steps, dt, R);
     for (int s = 0; s < steps && !st && !(c->fused && c->nranks == 1); ++s) {
         const int p = (parity + s) & 1;
         st = enqueue_step(c, Y[p], K[p], &c->ws[4], Y[p ^ 1], K[p ^ 1], nullptr, &c->d_rec[s],
@@ -1041,7 +1083,11 @@ static hsgn_status run_fixed_chunk(hsgn_ctx* c, int parity, int steps, double t,
         FixedGraph* fg = nullptr;
         if ((st = get_fixed_graph(c, steps, parity, dt, R, &fg))) return st;
         CK(cudaGraphLaunch(fg->exec, c->stream));
-        if (kernels) *kernels += (gauges ? steps : 0) + (c->fused == 2 ? steps : c->fused ? 2 * steps + 1 : 3 * steps);
+        if (kernels)
+            *kernels += (gauges ? steps : 0) + (c->fused == 2   ? steps
+                                                : c->fused == 3 ? 2 * steps
+                                                : c->fused == 1 ? 2 * steps + 1
+                                                                : 3 * steps);
     } else {
         hsgn_state* Y[2] = {&c->ws[0], &c->ws[1]};
         hsgn_state* K[2] = {&c->ws[2], &c->ws[3]};
@@ -1694,7 +1740,21 @@ extern "C" hsgn_status hsgn_profile_fused(hsgn_ctx* c, const hsgn_state* y, cons
     double acc = 0.0;
     for (int r = 0; r < reps; ++r) {
         CK(cudaEventRecord(e0, c->stream));
-        if (c->fused == 2)
+        if (c->fused == 3) {
+            StageArgs A = stage_args(c, MODE_S12, 0.0);
+            A.a = 0.5 * dt;
+            A.a2 = 0.75 * dt;
+            A.c1 = dt * (2.0 / 9.0);
+            A.c2 = dt * (1.0 / 3.0);
+            A.c3 = dt * (4.0 / 9.0);
+            A.y = c->ws[0].base;
+            A.k = c->ws[2].base;
+            A.out = c->ws[6].base;
+            A.bad = &c->d_rec[1].bad[0];
+            A.bad2 = &c->d_rec[1].bad[1];
+            A.minh = &c->d_rec[1].minh;
+            st = launch(c, MODE_S12, A);
+        } else if (c->fused == 2)
             st = enqueue_step_kernel(c, &c->ws[0], &c->ws[2], &c->ws[6], &c->ws[7], &c->d_rec[1], nullptr, dt);
         else
             st = enqueue_stage(c, 31, &c->ws[0], &c->ws[2], &c->ws[4], &c->ws[1], &c->ws[3], nullptr, &c->d_rec[1],

@@ -936,6 +936,178 @@ __global__ void __launch_bounds__(BX, HSGN_S31_MINB) sgn_s31_kernel(const StageA
     if (T.bad_b) atomicAdd(A.bad2, T.bad_b);
 }
 
+// y-quantities of the row above / below at this column for a finish at row
+// j: the ring entry of the neighbour row, or (clamped wall rows) the row's
+// own entry, as the unfused kernels' clamped stage input gives.
+__device__ __forceinline__ void ywin_prev(const StageArgs& A, int j, const double2* prev, const double2* cur, int tid,
+                                          YQ& Y) {
+    neighbour_y((j == 0 && A.y_lo == YE_CLAMP ? cur : prev) + tid, Y);
+}
+
+// ------------------------------------------------------------ fused S1 + S2
+// Stages 1 and 2 of one fixed step in one pass: reads y, k1 (= f(y)) and b,
+// writes ynew (+ min h): 128 B/node; stage 3 (k4 = f(ynew), 88 B/node)
+// follows as its own kernel, so a step moves 216 B/node.  S2 is the
+// HBM-heaviest stage (16 inputs); fusing S1 into it removes the k2 round
+// trip and the re-read of y and k1.  Pipeline per iteration r:
+//   P1  stage-1 input y + a1 k1 of row r -> ring A   |  barrier
+//   H1  k2 at row r-1; stage-2 input y + a2 k2 -> ring B, and
+//       ((y + c1 k1) + c2 k2) kept in registers for H2 of the next row
+//   H2  k3 at row r-2; ynew = part + c3 k3 (stored, min h)
+// Same tile / ring layout as S31 (WX2 = BX-4 columns, 2 x 3 slots x 4
+// pairs, 1/h in registers: 49 KB; 3 CTAs per SM at <= 168 registers).
+// Whole-grid contexts.
+// measured (r1, 8192^2): 3 CTAs/SM at <= 168 registers without spills runs
+// S12 in 3.16 ms; forcing 4 CTAs (128 registers) spills ~380 B/thread and
+// takes 7.1 ms.  Passing ring A's next-row y-quantities in registers and
+// issuing the next raw row before the barrier measured faster (3.16 vs 3.31).
+#ifndef HSGN_S12_MINB
+#define HSGN_S12_MINB (12 / (BX / 32))
+#endif
+#ifndef HSGN_S12_PASS_A
+#define HSGN_S12_PASS_A 1
+#endif
+#ifndef HSGN_S12_LATE_PF
+#define HSGN_S12_LATE_PF 0
+#endif
+
+template <int KIND>
+__global__ void __launch_bounds__(BX, HSGN_S12_MINB) sgn_s12_kernel(const StageArgs A, const KPtrs P) {
+    extern __shared__ __align__(16) double2 ring[];  // ring A | ring B, each 3 x NPF x BX
+    __shared__ unsigned long long s_min[BX / 32];
+    __shared__ int s_skip;
+    const int tid = threadIdx.x;
+    if (A.halt) {  // failure protocol: the previous step's S3 counter and min h
+        if (tid == 0) {
+            int skip = *A.halt;
+            if (!skip && A.chk_bad && *A.chk_bad) skip = 1;
+            if (!skip && A.chk_minh) {
+                const unsigned long long mb = *A.chk_minh;
+                if (mb != ~0ull && __longlong_as_double((long long)mb) <= A.h_floor) skip = 1;
+            }
+            if (skip) *A.halt = 1;
+            s_skip = skip;
+        }
+        __syncthreads();
+        if (s_skip) return;
+    }
+    const int nx = A.nx, ny = A.ny;
+    const int i = (int)blockIdx.x * WX2 - 2 + tid;
+    const bool fa = tid >= 1 && tid <= BX - 2 && i >= -1 && i <= nx;  // stage-1 finish
+    const bool fb = tid >= 2 && tid <= BX - 3 && i >= 0 && i < nx;    // stage-2 finish (owned column)
+    int c = i;
+    if (i < 0) c = A.x_bounded ? 0 : nx + i;
+    if (i >= nx) c = (A.x_bounded || i > nx + 1) ? nx - 1 : i - nx;
+    const unsigned col = (unsigned)c;
+    const bool xl = A.x_bounded && i == 0, xr = A.x_bounded && i == nx - 1;
+    const double cx = (xl || xr) ? A.c1x : A.cpx;
+    const int sl = xl ? tid : tid - 1, sr = xr ? tid : tid + 1;
+    const int j0 = A.band0 + blockIdx.y * A.rows_per_block;
+    const int j1 = min(A.band1 > 0 ? A.band1 : ny, j0 + A.rows_per_block);
+    const int jc0 = A.y_lo == YE_CLAMP ? 0 : INT_MIN, jc1 = A.y_hi == YE_CLAMP ? ny - 1 : INT_MIN;
+    const bool clamp_hi = A.y_hi == YE_CLAMP;
+    const unsigned unx = (unsigned)nx;
+    unsigned long long bad1 = 0, bad2 = 0, my_min = ~0ull;
+
+    constexpr int SLOT = NPF * BX;
+    // at iteration r ring A holds rows (r-2, r-1, r) in (pa, pb, pc), ring B
+    // rows (r-3, r-2, r-1) in (qa, qb, qc); pc and qc are written now
+    double2 *pa = ring, *pb = ring + SLOT, *pc = ring + 2 * SLOT;
+    double2 *qa = ring + 3 * SLOT, *qb = ring + 4 * SLOT, *qc = ring + 5 * SLOT;
+    double rhap = 0.0, rhbp = 0.0;  // 1/h of ring A row r-1 / ring B row r-2
+    double partp[5];                // ((y + c1 k1) + c2 k2) of row r-2
+#pragma unroll
+    for (int f = 0; f < 5; ++f) partp[f] = 0.0;
+
+    Raw raw;
+    load_raw<MODE_S1>(P, (unsigned)map_row2(A, j0 - 2) * unx + col, raw);
+#pragma unroll 1
+    for (int r = j0 - 2; r <= j1 + 1; ++r) {
+        // ---- P1: stage-1 input of row r (raw of row r+1 loaded right after)
+        YQ ya;
+        double rhac;
+        {
+            const bool ok = products<MODE_S1, false>(A, raw, pc + tid, ya, &rhac);
+            if (fb && r >= j0 && r < j1 && !ok) ++bad1;
+        }
+        if (!HSGN_S12_LATE_PF && r + 1 <= j1 + 1) load_raw<MODE_S1>(P, (unsigned)map_row2(A, r + 1) * unx + col, raw);
+        __syncthreads();
+        // ---- H1: k2 at row r-1 -> stage-2 input -> ring B (qc)
+        YQ yb;
+        double rhbc = 0.0, partc[5];
+        if (r - 1 >= j0 - 1 && fa) {
+            const int j = r - 1;
+            // y, k1 of row j again (this thread loaded them one row ago: L1/L2)
+            const unsigned offj = (unsigned)map_row2(A, j) * unx + col;
+            double yj[5], kj[5];
+#pragma unroll
+            for (int f = 0; f < 5; ++f) {
+                yj[f] = __ldg(P.y[f] + offj);
+                kj[f] = __ldg(P.k[f] + offj);
+            }
+            YQ yp, yc;
+            ywin_prev(A, j, pa, pb, tid, yp);
+            const bool hi = clamp_hi && j == ny - 1;
+            if (hi || !HSGN_S12_PASS_A) neighbour_y((hi ? pb : pc) + tid, yc);
+            const double cy = (j == jc0 || j == jc1) ? A.c1y : A.cpy;
+            double k2[5];
+            tendency<KIND>(A, pb, tid, sl, sr, cx, cy, xl, xr, i, j, yp, (hi || !HSGN_S12_PASS_A) ? yc : ya, rhap,
+                           k2);
+            double q[5];
+#pragma unroll
+            for (int f = 0; f < 5; ++f) {
+                q[f] = dadd(yj[f], dmul(A.a2, k2[f]));                                  // state_add1
+                partc[f] = dadd(dadd(yj[f], dmul(A.c1, kj[f])), dmul(A.c2, k2[f]));  // state_add3, 2 terms
+            }
+            const bool ok = products_q<false>(q, pb[tid + P_EB * BX].y, qc + tid, yb, &rhbc);
+            if (fb && j >= j0 && j < j1 && !ok) ++bad2;
+        }
+        if (HSGN_S12_LATE_PF && r + 1 <= j1 + 1) load_raw<MODE_S1>(P, (unsigned)map_row2(A, r + 1) * unx + col, raw);
+        // ---- H2: k3 at row r-2 -> ynew (stored, min h)
+        if (r - 2 >= j0 && fb) {
+            const int j = r - 2;
+            YQ yp, yc;
+            ywin_prev(A, j, qa, qb, tid, yp);
+            const bool hi = clamp_hi && j == ny - 1;
+            if (hi) neighbour_y(qb + tid, yc);
+            const double cy = (j == jc0 || j == jc1) ? A.c1y : A.cpy;
+            double k3[5];
+            tendency<KIND>(A, qb, tid, sl, sr, cx, cy, xl, xr, i, j, yp, hi ? yc : yb, rhbp, k3);
+            const unsigned off = (unsigned)(j + 1) * unx + col;
+#pragma unroll
+            for (int f = 0; f < 5; ++f) P.out[f][off] = dadd(partp[f], dmul(A.c3, k3[f]));  // state_add3
+            const unsigned long long bits =
+                (unsigned long long)__double_as_longlong(dadd(partp[0], dmul(A.c3, k3[0])));
+            my_min = bits < my_min ? bits : my_min;
+        }
+        // ---- rotate
+        double2* t = pa;
+        pa = pb;
+        pb = pc;
+        pc = t;
+        t = qa;
+        qa = qb;
+        qb = qc;
+        qc = t;
+        rhap = rhac;
+        rhbp = rhbc;
+#pragma unroll
+        for (int f = 0; f < 5; ++f) partp[f] = partc[f];
+    }
+    if (bad1) atomicAdd(A.bad, bad1);
+    if (bad2) atomicAdd(A.bad2, bad2);
+    if (A.minh) {
+        const unsigned long long m = warp_min_u64(my_min);
+        if ((tid & 31) == 0) s_min[tid >> 5] = m;
+        __syncthreads();
+        if (tid == 0) {
+            unsigned long long mm = s_min[0];
+            for (int k = 1; k < BX / 32; ++k) mm = s_min[k] < mm ? s_min[k] : mm;
+            if (mm != ~0ull) atomicMin(A.minh, mm);
+        }
+    }
+}
+
 // ------------------------------------------------------------ whole step
 // One fixed BS3 step in one pass (whole-grid contexts): reads y, k1 (= f(y),
 // FSAL) and b, writes ynew and k4 = f(ynew): 168 B/node per step.  The three
@@ -958,14 +1130,6 @@ constexpr int WX3 = BX - 6;
 #ifndef HSGN_STEP_MINB
 #define HSGN_STEP_MINB (12 / (BX / 32))  // 12 warps per SM (3 x 72 KB of rings)
 #endif
-
-// y-quantities of the row above / below at this column for a finish at row
-// j: the ring entry of the neighbour row, or (clamped wall rows) the row's
-// own entry, as the unfused kernels' clamped stage input gives.
-__device__ __forceinline__ void ywin_prev(const StageArgs& A, int j, const double2* prev, const double2* cur, int tid,
-                                          YQ& Y) {
-    neighbour_y((j == 0 && A.y_lo == YE_CLAMP ? cur : prev) + tid, Y);
-}
 
 template <int KIND>
 __global__ void __launch_bounds__(BX, HSGN_STEP_MINB) sgn_step_kernel(const StageArgs A, const KPtrs P) {
@@ -1261,8 +1425,34 @@ static cudaError_t launch_step(const StageArgs& A, cudaStream_t st) {
 }
 
 template <int KIND>
+static cudaError_t launch_s12(const StageArgs& A, cudaStream_t st) {
+    constexpr size_t bytes = sizeof(double2) * 2 * 3 * NPF * BX;
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e =
+            cudaFuncSetAttribute(sgn_s12_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    KPtrs P;
+    const long long g = A.nx;
+    for (int f = 0; f < 5; ++f) {
+        P.y[f] = A.y + f * A.fs - g;
+        P.k[f] = A.k + f * A.fs - g;
+        P.kc[f] = P.yold[f] = nullptr;
+        P.part[f] = P.out2[f] = nullptr;
+        P.out[f] = A.out + f * A.fs - g;
+    }
+    P.b = A.b - g;
+    dim3 grid((A.nx + WX2 - 1) / WX2, (band_rows(A) + A.rows_per_block - 1) / A.rows_per_block);
+    sgn_s12_kernel<KIND><<<grid, BX, bytes, st>>>(A, P);
+    return cudaGetLastError();
+}
+
+template <int KIND>
 static cudaError_t launch_kind(int mode, const StageArgs& A, cudaStream_t st) {
     switch (mode) {
+        case MODE_S12: return launch_s12<KIND>(A, st);
         case MODE_STEP: return launch_step<KIND>(A, st);
         case MODE_S31: return launch_s31<KIND>(A, st);
         case MODE_RHS: return launch_mode<MODE_RHS, KIND>(A, st);

@@ -48,7 +48,7 @@ def test_fused_fixed_steps_bitwise(orc, nx, ny, kx, ky, rpb):
     g, ctx = _ctx(og, b)
     if rpb:
         ctx.set_rows_per_block(rpb)
-    for mode in (0, 1, 2):
+    for mode in (0, 1, 2, 3):
         ctx.fused_stages = mode
         assert ctx.fused_stages == mode
         res = H.adaptive_solve(ctx, H.StateField(g, q), 0.0, T, H.IntegratorConfig(fixed_dt=dt))
@@ -70,7 +70,7 @@ def _drying_state(nx, ny, amp, U):
 @pytest.mark.parametrize("amp,U,dt,floor", [(0.99, 10.0, 1e-3, 1e-12), (0.99, 30.0, 1e-3, 1e-12),
                                              (0.99, 10.0, 1e-3, 0.005), (0.999, 10.0, 1e-3, 0.005),
                                              (0.99, 10.0, 3e-3, 1e-12)])
-@pytest.mark.parametrize("fused", [0, 1, 2])
+@pytest.mark.parametrize("fused", [0, 1, 2, 3])
 def test_fixed_step_failures_match_reference(orc, amp, U, dt, floor, fused):
     nx, ny = 64, 48
     og = omake_grid(nx, ny)
@@ -99,7 +99,7 @@ def test_fused_launch_count_and_profile():
     y = ctx.state(H.StateField(g, q))
     k1 = ctx.state()
     H.rhs(ctx, 0.0, y, k1)
-    for mode, want in ((1, 2 * 64 + 1), (0, 3 * 64), (2, 64)):
+    for mode, want in ((1, 2 * 64 + 1), (0, 3 * 64), (2, 64), (3, 2 * 64)):
         ctx.fused_stages = mode
         done, ms, kernels = H.bs3_fixed_steps(ctx, y, k1, 0.0, 1e-5, 64)
         assert done == 64 and kernels == want, mode

@@ -16,12 +16,12 @@ ctx = H.make_rhs_context(g, H.PhysSetup(9.81, lam, 1e-12, b.reshape(n, n)), devi
 y = ctx.state(q)
 k1 = ctx.state()
 H.rhs(ctx, 0.0, y, k1)
-for mode in (0, 1, 2):
+for mode in (0, 1, 2, 3):
     ctx.fused_stages = mode
     H.bs3_fixed_steps(ctx, y, k1, 0.0, dt, steps)  # capture + warm
 for rep in range(reps):
     line = []
-    for mode in (0, 1, 2):
+    for mode in (0, 1, 2, 3):
         ctx.fused_stages = mode
         H.bs3_fixed_steps(ctx, y, k1, 0.0, dt, 4)
         done, ms, kern = H.bs3_fixed_steps(ctx, y, k1, 0.0, dt, steps)
