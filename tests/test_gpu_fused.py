@@ -103,3 +103,26 @@ def test_fused_launch_count_and_profile():
         ctx.fused_stages = mode
         done, ms, kernels = H.bs3_fixed_steps(ctx, y, k1, 0.0, 1e-5, 64)
         assert done == 64 and kernels == want, mode
+
+
+@pytest.mark.parametrize("kind", [0, 1])
+def test_fused_structures_deterministic_under_repetition(kind):
+    """Race detection by repetition (compute-sanitizer is unavailable on this
+    pool): every kernel structure, 12 repetitions of 6 steps on a grid with
+    partial tiles and short row strips, must give one bit pattern."""
+    nx, ny = 1000, 300
+    og = omake_grid(nx, ny, kind_x=kind, kind_y=kind)
+    q, b = mms_exact_field(og, 0.3)
+    g, ctx = _ctx(og, b)
+    ctx.set_rows_per_block(5)
+    dx = 2.0 / (nx - 1 if kind else nx)
+    dt = 0.25 * dx / 20.0
+    first = None
+    for rep in range(12):
+        for mode in (0, 1, 2, 3):
+            ctx.fused_stages = mode
+            res = H.adaptive_solve(ctx, H.StateField(g, q), 0.0, 6 * dt, H.IntegratorConfig(fixed_dt=dt))
+            flat = res.q.flat().copy()
+            if first is None:
+                first = flat
+            assert _neq(flat, first) == 0, (rep, mode)
