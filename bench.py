@@ -39,6 +39,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 BYTES_PER_NODE = {"S1": 128, "S2": 168, "S3": 88, "S31": 128, "STEP": 168, "S12": 128}
+BYTES_PER_POINT_STAGE = 128  # unfused step: 384 B per node / 3 stages
 # FP64 instructions (DADD + DMUL + DFMA) per node of each kernel, from the ncu
 # SASS mixes in profiles/ (r1_sass_mix_stage_kernels.txt, r1f_sass_mix_s31.txt,
 # r1g_sass_mix_s12.txt): the compute roofline of the FP64-issue-bound kernels
@@ -290,6 +291,12 @@ def main():
                 "bytes_per_node": BYTES_PER_NODE[names[dom]], "peak_source": peak_kind,
                 "stage_ms": {names[k]: ms3[k] for k in range(len(names))},
                 "step_bytes_per_node": step_bytes_per_node(mode, min(64, args.steps)),
+                # updates/s x 128 B (the unfused compulsory traffic per
+                # point-stage) against the HBM peak; fusion removes traffic, so this
+                # equivalent-bandwidth fraction exceeds the fused kernels' own
+                "equiv_unfused": {"bytes_per_point_stage": BYTES_PER_POINT_STAGE,
+                                  "achieved": value * BYTES_PER_POINT_STAGE / 1e9,
+                                  "frac": value * BYTES_PER_POINT_STAGE / 1e9 / peak},
                 "step_gbs": step_bytes_per_node(mode, min(64, args.steps)) * points / (ms / args.steps * 1e-3) / 1e9}
 
     # end-to-end through the public API with host buffers (pinned)
