@@ -87,8 +87,9 @@ hsgn_status hsgn_ctx_create(const hsgn_grid* grid, const hsgn_phys* phys, const 
                             int device, hsgn_ctx** out);
 
 /* Slab of a y-decomposed grid (multi-GPU): rows
- * [j_begin, j_end) of the global grid live on this rank; b_host holds the
- * slab's rows only.  Neighbour ranks are (rank-1, rank+1) mod nranks. */
+ * [j_begin, j_end) of the global grid (at least 2) live on this rank; b_host
+ * holds the slab's rows only.  Neighbour ranks are (rank-1, rank+1) mod
+ * nranks. */
 hsgn_status hsgn_ctx_create_slab(const hsgn_grid* grid, const hsgn_phys* phys, const double* b_host,
                                  int device, int32_t j_begin, int32_t j_end, int32_t rank,
                                  int32_t nranks, hsgn_ctx** out);
@@ -143,8 +144,8 @@ hsgn_status hsgn_state_free(hsgn_ctx* ctx, hsgn_state* s);
 hsgn_status hsgn_state_upload(hsgn_ctx* ctx, hsgn_state* s, const double* host);
 hsgn_status hsgn_state_download(hsgn_ctx* ctx, const hsgn_state* s, double* host);
 hsgn_status hsgn_state_copy(hsgn_ctx* ctx, const hsgn_state* src, hsgn_state* dst);
-/* Device pointer of field f, row 0 (row pitch = nx doubles; rows -1 and
- * ny_local are the ghost rows). */
+/* Device pointer of field f, row 0 (row pitch = nx doubles; rows -2, -1
+ * and ny_local, ny_local + 1 are the ghost rows). */
 hsgn_status hsgn_state_field_ptr(const hsgn_state* s, int32_t f, double** out);
 
 /* ------------------------------------------------------------ operators */

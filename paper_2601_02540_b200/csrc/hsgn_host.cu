@@ -228,7 +228,7 @@ hsgn_status alloc_state(hsgn_ctx* c, hsgn_state* s) {
     s->fs = c->fs;
     CK(cudaMalloc(&s->base, sizeof(double) * 5 * c->fs));
     CK(cudaMemsetAsync(s->base, 0, sizeof(double) * 5 * c->fs, c->stream));
-    s->base += c->grid.nx;  // row 0 of field 0 (row -1 is the ghost row)
+    s->base += GHOST * c->grid.nx;  // row 0 of field 0 (rows -GHOST..-1 are ghost rows)
     return HSGN_OK;
 }
 
@@ -236,7 +236,7 @@ hsgn_status alloc_state(hsgn_ctx* c, hsgn_state* s) {
 
 // Freed pointer must be the allocation base (row -1 of field 0).
 static void free_state_c(hsgn_ctx* c, hsgn_state* s) {
-    if (s->base) cudaFree(s->base - c->grid.nx);
+    if (s->base) cudaFree(s->base - GHOST * c->grid.nx);
     s->base = nullptr;
 }
 
@@ -245,7 +245,7 @@ static hsgn_status setup_ctx(hsgn_ctx* c) {
     c->dx = spacing(g.x_min, g.x_max, g.nx, g.kind_x);
     c->dy = spacing(g.y_min, g.y_max, g.ny, g.kind_y);
     c->ny_loc = c->j_end - c->j_begin;
-    c->fs = (long long)(c->ny_loc + 2) * g.nx;
+    c->fs = (long long)(c->ny_loc + 2 * GHOST) * g.nx;
     StageArgs& A = c->base;
     std::memset(&A, 0, sizeof A);
     A.nx = g.nx;
@@ -313,10 +313,11 @@ static hsgn_status setup_ctx(hsgn_ctx* c) {
 
 // ------------------------------------------------------------------ halo exchange
 
-// After a stage wrote `s` (rows 0..ny_loc-1), fill the neighbours' ghost rows:
-// send row 0 to rank-1 (its row ny_loc ghost) and row ny_loc-1 to rank+1;
-// receive into our rows -1 / ny_loc.  One grouped NCCL call per exchange, on
-// the context stream (graph-capturable).
+// After a kernel wrote `s` (rows 0..ny_loc-1), fill the neighbours' ghost
+// rows: send rows 0..GHOST-1 to rank-1 (its upper ghost rows) and the last
+// GHOST rows to rank+1; receive into our rows -GHOST..-1 / ny_loc..ny_loc+
+// GHOST-1.  One grouped NCCL call per exchange, on the context stream
+// (graph-capturable).
 static hsgn_status exchange(hsgn_ctx* c, const hsgn_state* s, int nfields) {
     if (c->nranks == 1 || c->in_group) return HSGN_OK;  // in a group the driver pulls halos
     if (!c->comm) return fail(c, HSGN_ENCCL, "slab context has no NCCL communicator attached");
@@ -328,13 +329,14 @@ static hsgn_status exchange(hsgn_ctx* c, const hsgn_state* s, int nfields) {
     int r = N.group_start();
     for (int f = 0; f < nfields && r == 0; ++f) {
         double* fld = s->f(f);
+        const size_t span = (size_t)GHOST * nx;  // GHOST contiguous rows per field and direction
         if (dn >= 0) {
-            r |= N.send(fld, nx, NCCL_FLOAT64, dn, c->comm, c->stream);
-            r |= N.recv(fld - nx, nx, NCCL_FLOAT64, dn, c->comm, c->stream);
+            r |= N.send(fld, span, NCCL_FLOAT64, dn, c->comm, c->stream);
+            r |= N.recv(fld - span, span, NCCL_FLOAT64, dn, c->comm, c->stream);
         }
         if (up >= 0) {
-            r |= N.send(fld + (long long)(c->ny_loc - 1) * nx, nx, NCCL_FLOAT64, up, c->comm, c->stream);
-            r |= N.recv(fld + (long long)c->ny_loc * nx, nx, NCCL_FLOAT64, up, c->comm, c->stream);
+            r |= N.send(fld + (long long)(c->ny_loc - GHOST) * nx, span, NCCL_FLOAT64, up, c->comm, c->stream);
+            r |= N.recv(fld + (long long)c->ny_loc * nx, span, NCCL_FLOAT64, up, c->comm, c->stream);
         }
     }
     r |= N.group_end();
@@ -522,6 +524,42 @@ static hsgn_status enqueue_chunk_step(hsgn_ctx* c, int parity, int steps, double
 }
 
 // A chunk of `steps` fixed steps as S12 (stages 1+2) + S3 per step.
+// One fixed step as S12 (stages 1+2: y, k1 -> ynew) then S3 (k4 = f(ynew)),
+// each followed by the slab halo exchange of its output (no-op on a whole
+// grid; in an in-process group the driver pulls instead: pass `group`).
+static hsgn_status enqueue_s12(hsgn_ctx* c, const hsgn_state* y, const hsgn_state* k1, hsgn_state* ynew,
+                               StepRec* rec, const StepRec* prev, double dt) {
+    StageArgs A = stage_args(c, MODE_S12, 0.0);
+    A.a = 0.5 * dt;
+    A.a2 = 0.75 * dt;
+    A.c1 = dt * (2.0 / 9.0);
+    A.c2 = dt * (1.0 / 3.0);
+    A.c3 = dt * (4.0 / 9.0);
+    A.y = y->base;
+    A.k = k1->base;
+    A.out = ynew->base;
+    A.bad = &rec->bad[0];
+    A.bad2 = &rec->bad[1];
+    A.minh = &rec->minh;
+    A.halt = c->d_halt;
+    A.chk_bad = prev ? &prev->bad[2] : nullptr;
+    A.chk_minh = prev ? &prev->minh : nullptr;
+    return launch(c, MODE_S12, A);
+}
+
+static hsgn_status enqueue_s3_fixed(hsgn_ctx* c, const hsgn_state* ynew, hsgn_state* k4, StepRec* rec, double dt) {
+    StageArgs A = stage_args(c, MODE_S3, dt);  // k4 = f(ynew), FSAL
+    A.y = ynew->base;
+    A.out = k4->base;
+    A.bad = &rec->bad[2];
+    A.halt = c->d_halt;
+    A.chk_bad = &rec->bad[1];
+    A.chk_bad2 = &rec->bad[0];
+    return launch(c, MODE_S3, A);
+}
+
+// A chunk of `steps` fixed steps as S12 + S3 per step (+1 gauge gather per
+// step with a recorder; slab halo exchanges after each kernel).
 static hsgn_status enqueue_chunk_s12(hsgn_ctx* c, int parity, int steps, double dt, const hsgn_recorder* R) {
     hsgn_state* Y[2] = {&c->ws[0], &c->ws[1]};
     hsgn_state* K[2] = {&c->ws[2], &c->ws[3]};
@@ -530,34 +568,13 @@ static hsgn_status enqueue_chunk_s12(hsgn_ctx* c, int parity, int steps, double 
     for (int s = 0; s < steps; ++s) {
         const int p = (parity + s) & 1;
         StepRec* rec = &c->d_rec[s];
-        const StepRec* prev = s ? &c->d_rec[s - 1] : nullptr;
-        StageArgs A = stage_args(c, MODE_S12, 0.0);
-        A.a = 0.5 * dt;
-        A.a2 = 0.75 * dt;
-        A.c1 = dt * (2.0 / 9.0);
-        A.c2 = dt * (1.0 / 3.0);
-        A.c3 = dt * (4.0 / 9.0);
-        A.y = Y[p]->base;
-        A.k = K[p]->base;
-        A.out = Y[p ^ 1]->base;
-        A.bad = &rec->bad[0];
-        A.bad2 = &rec->bad[1];
-        A.minh = &rec->minh;
-        A.halt = c->d_halt;
-        A.chk_bad = prev ? &prev->bad[2] : nullptr;
-        A.chk_minh = prev ? &prev->minh : nullptr;
-        if ((st = launch(c, MODE_S12, A))) return st;
+        if ((st = enqueue_s12(c, Y[p], K[p], Y[p ^ 1], rec, s ? &c->d_rec[s - 1] : nullptr, dt))) return st;
+        if ((st = exchange(c, Y[p ^ 1], 5))) return st;
         if (gauges)
             CK(launch_gauges(Y[p ^ 1]->base, c->b, R->d_idx, (int)R->gi.size(),
                              R->d_gauge + (size_t)s * R->gi.size(), c->stream));
-        A = stage_args(c, MODE_S3, dt);  // k4 = f(ynew), FSAL
-        A.y = Y[p ^ 1]->base;
-        A.out = K[p ^ 1]->base;
-        A.bad = &rec->bad[2];
-        A.halt = c->d_halt;
-        A.chk_bad = &rec->bad[1];
-        A.chk_bad2 = &rec->bad[0];
-        if ((st = launch(c, MODE_S3, A))) return st;
+        if ((st = enqueue_s3_fixed(c, Y[p ^ 1], K[p ^ 1], rec, dt))) return st;
+        if ((st = exchange(c, K[p ^ 1], 5))) return st;
     }
     return HSGN_OK;
 }
@@ -716,7 +733,7 @@ static hsgn_status create_common(const hsgn_grid* grid, const hsgn_phys* phys, c
     if (!(grid->x_max > grid->x_min) || !(grid->y_max > grid->y_min))
         return bad_arg("make_grid: domain extents must be increasing");
     if (grid->nx < 4 || grid->ny < 4) return bad_arg("make_grid: need at least 4 nodes per direction");
-    if (nranks < 1 || rank < 0 || rank >= nranks || j_begin < 0 || j_end > grid->ny || j_end - j_begin < 2)
+    if (nranks < 1 || rank < 0 || rank >= nranks || j_begin < 0 || j_end > grid->ny || j_end - j_begin < GHOST)
         return bad_arg("invalid slab");
     c->j_begin = j_begin;
     c->j_end = j_end;
@@ -732,10 +749,10 @@ static hsgn_status create_common(const hsgn_grid* grid, const hsgn_phys* phys, c
         return HSGN_ECUDA;
     }
     const int ny_loc = j_end - j_begin;
-    const long long fsz = (long long)(ny_loc + 2) * grid->nx;
+    const long long fsz = (long long)(ny_loc + 2 * GHOST) * grid->nx;
     e = cudaMalloc(&c->b_alloc, sizeof(double) * fsz);
     if (e == cudaSuccess) {
-        c->b = c->b_alloc + grid->nx;
+        c->b = c->b_alloc + GHOST * grid->nx;
         e = cudaMemcpyAsync(c->b, b_host, sizeof(double) * ny_loc * grid->nx, cudaMemcpyHostToDevice, c->stream);
     }
     if (e == cudaSuccess) e = cudaEventCreate(&c->ev0);
@@ -918,7 +935,7 @@ hsgn_status hsgn_state_download(hsgn_ctx* c, const hsgn_state* s, double* host) 
 
 hsgn_status hsgn_state_copy(hsgn_ctx* c, const hsgn_state* src, hsgn_state* dst) {
     if (!c || !src || !dst) return HSGN_EINVAL;
-    CK(cudaMemcpyAsync(dst->base - c->grid.nx, src->base - c->grid.nx, sizeof(double) * 5 * c->fs,
+    CK(cudaMemcpyAsync(dst->base - GHOST * c->grid.nx, src->base - GHOST * c->grid.nx, sizeof(double) * 5 * c->fs,
                        cudaMemcpyDeviceToDevice, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     return HSGN_OK;
@@ -1088,6 +1105,12 @@ static hsgn_status run_fixed_chunk(hsgn_ctx* c, int parity, int steps, double t,
                                                 : c->fused == 3 ? 2 * steps
                                                 : c->fused == 1 ? 2 * steps + 1
                                                                 : 3 * steps);
+    } else if (c->source == 0 && c->fused == 3 && !gauges) {
+        // slab context: the fused structure with NCCL halo exchanges between
+        // the kernels (direct launches)
+        reset_recs(c, steps);
+        if ((st = enqueue_chunk_s12(c, parity, steps, dt, nullptr))) return st;
+        if (kernels) *kernels += 2 * steps;
     } else {
         hsgn_state* Y[2] = {&c->ws[0], &c->ws[1]};
         hsgn_state* K[2] = {&c->ws[2], &c->ws[3]};
@@ -1247,7 +1270,7 @@ extern "C" hsgn_status hsgn_solve_recorded(hsgn_ctx* c, const hsgn_state* q0, do
     if ((st = ensure_ws(c, CHUNK))) return st;
     c->base.h_floor = cfg->h_floor;  // the stage kernels' halt test and the chunk scan use the run's floor
     auto copy_state = [&](const hsgn_state* src, hsgn_state* dst) -> hsgn_status {
-        CK(cudaMemcpyAsync(dst->base - c->grid.nx, src->base - c->grid.nx, sizeof(double) * 5 * c->fs,
+        CK(cudaMemcpyAsync(dst->base - GHOST * c->grid.nx, src->base - GHOST * c->grid.nx, sizeof(double) * 5 * c->fs,
                            cudaMemcpyDeviceToDevice, c->stream));
         return HSGN_OK;
     };
@@ -1596,9 +1619,9 @@ extern "C" hsgn_status hsgn_bs3_fixed_steps(hsgn_ctx* c, hsgn_state* y, hsgn_sta
     if ((st = ensure_ws(c, CHUNK))) return st;
     c->base.h_floor = c->phys.h_floor;
     // y, k1 are caller buffers: run in the workspace pair and copy back
-    CK(cudaMemcpyAsync(c->ws[0].base - c->grid.nx, y->base - c->grid.nx, sizeof(double) * 5 * c->fs,
+    CK(cudaMemcpyAsync(c->ws[0].base - GHOST * c->grid.nx, y->base - GHOST * c->grid.nx, sizeof(double) * 5 * c->fs,
                        cudaMemcpyDeviceToDevice, c->stream));
-    CK(cudaMemcpyAsync(c->ws[2].base - c->grid.nx, k1->base - c->grid.nx, sizeof(double) * 5 * c->fs,
+    CK(cudaMemcpyAsync(c->ws[2].base - GHOST * c->grid.nx, k1->base - GHOST * c->grid.nx, sizeof(double) * 5 * c->fs,
                        cudaMemcpyDeviceToDevice, c->stream));
     int p = 0;
     int64_t done_total = 0, kernels = 0;
@@ -1641,9 +1664,9 @@ extern "C" hsgn_status hsgn_bs3_fixed_steps(hsgn_ctx* c, hsgn_state* y, hsgn_sta
         }
     }
     CK(cudaEventRecord(c->ev1, c->stream));
-    CK(cudaMemcpyAsync(y->base - c->grid.nx, c->ws[p].base - c->grid.nx, sizeof(double) * 5 * c->fs,
+    CK(cudaMemcpyAsync(y->base - GHOST * c->grid.nx, c->ws[p].base - GHOST * c->grid.nx, sizeof(double) * 5 * c->fs,
                        cudaMemcpyDeviceToDevice, c->stream));
-    CK(cudaMemcpyAsync(k1->base - c->grid.nx, c->ws[2 + p].base - c->grid.nx, sizeof(double) * 5 * c->fs,
+    CK(cudaMemcpyAsync(k1->base - GHOST * c->grid.nx, c->ws[2 + p].base - GHOST * c->grid.nx, sizeof(double) * 5 * c->fs,
                        cudaMemcpyDeviceToDevice, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     float ms = 0.f;
@@ -1664,9 +1687,9 @@ extern "C" hsgn_status hsgn_profile_stages(hsgn_ctx* c, const hsgn_state* y, con
     CK(cudaSetDevice(c->device));
     hsgn_status st;
     if ((st = ensure_ws(c, 1))) return st;
-    CK(cudaMemcpyAsync(c->ws[0].base - c->grid.nx, y->base - c->grid.nx, sizeof(double) * 5 * c->fs,
+    CK(cudaMemcpyAsync(c->ws[0].base - GHOST * c->grid.nx, y->base - GHOST * c->grid.nx, sizeof(double) * 5 * c->fs,
                        cudaMemcpyDeviceToDevice, c->stream));
-    CK(cudaMemcpyAsync(c->ws[2].base - c->grid.nx, k1->base - c->grid.nx, sizeof(double) * 5 * c->fs,
+    CK(cudaMemcpyAsync(c->ws[2].base - GHOST * c->grid.nx, k1->base - GHOST * c->grid.nx, sizeof(double) * 5 * c->fs,
                        cudaMemcpyDeviceToDevice, c->stream));
     cudaEvent_t ev[4];
     for (int k = 0; k < 4; ++k) CK(cudaEventCreate(&ev[k]));
@@ -1725,9 +1748,9 @@ extern "C" hsgn_status hsgn_profile_fused(hsgn_ctx* c, const hsgn_state* y, cons
     CK(cudaSetDevice(c->device));
     hsgn_status st;
     if ((st = ensure_ws(c, 2))) return st;
-    CK(cudaMemcpyAsync(c->ws[0].base - c->grid.nx, y->base - c->grid.nx, sizeof(double) * 5 * c->fs,
+    CK(cudaMemcpyAsync(c->ws[0].base - GHOST * c->grid.nx, y->base - GHOST * c->grid.nx, sizeof(double) * 5 * c->fs,
                        cudaMemcpyDeviceToDevice, c->stream));
-    CK(cudaMemcpyAsync(c->ws[2].base - c->grid.nx, k1->base - c->grid.nx, sizeof(double) * 5 * c->fs,
+    CK(cudaMemcpyAsync(c->ws[2].base - GHOST * c->grid.nx, k1->base - GHOST * c->grid.nx, sizeof(double) * 5 * c->fs,
                        cudaMemcpyDeviceToDevice, c->stream));
     reset_recs(c, 2);
     for (int stage = 1; stage <= 2; ++stage)
@@ -1829,14 +1852,14 @@ hsgn_status group_pull(hsgn_group* G, const std::vector<hsgn_state*>& parts, int
         const int dn = g_dn(G, r), up = g_up(G, r);
         cudaSetDevice(c->device);
         HaloPull H;
-        H.nx = G->grid.nx;
+        H.nx = GHOST * G->grid.nx;  // GHOST contiguous rows per field and direction
         H.count = 0;
         const long long nx = G->grid.nx;
         for (int f = 0; f < nf; ++f) {
             if (dn >= 0) {
                 const hsgn_ctx* d = G->m[dn];
-                H.dst[H.count] = parts[r]->f(f) - nx;
-                H.src[H.count] = parts[dn]->f(f) + (long long)(d->ny_loc - 1) * nx;
+                H.dst[H.count] = parts[r]->f(f) - GHOST * nx;
+                H.src[H.count] = parts[dn]->f(f) + (long long)(d->ny_loc - GHOST) * nx;
                 ++H.count;
             }
             if (up >= 0) {
@@ -2049,9 +2072,9 @@ hsgn_status hsgn_group_bs3_fixed_steps(hsgn_group* G, hsgn_gstate* y, hsgn_gstat
         K2[r] = &c->ws[4];
         cudaSetDevice(c->device);
         group_wait_pulls(G, r);
-        cudaMemcpyAsync(c->ws[0].base - c->grid.nx, y->p[r]->base - c->grid.nx, sizeof(double) * 5 * c->fs,
+        cudaMemcpyAsync(c->ws[0].base - GHOST * c->grid.nx, y->p[r]->base - GHOST * c->grid.nx, sizeof(double) * 5 * c->fs,
                         cudaMemcpyDeviceToDevice, c->stream);
-        cudaMemcpyAsync(c->ws[2].base - c->grid.nx, k1->p[r]->base - c->grid.nx, sizeof(double) * 5 * c->fs,
+        cudaMemcpyAsync(c->ws[2].base - GHOST * c->grid.nx, k1->p[r]->base - GHOST * c->grid.nx, sizeof(double) * 5 * c->fs,
                         cudaMemcpyDeviceToDevice, c->stream);
         cudaEventRecord(G->evk[r], c->stream);
         cudaEventRecord(G->evp[r], c->stream);
@@ -2059,19 +2082,28 @@ hsgn_status hsgn_group_bs3_fixed_steps(hsgn_group* G, hsgn_gstate* y, hsgn_gstat
     int p = 0;
     int64_t done = 0;
     hsgn_status result = HSGN_OK;
+    // the members' fixed-step structure: S12 + S3 (kernels 1, 2) or one
+    // kernel per stage (kernels 1..3); halos pulled after every kernel
+    const bool s12 = G->m[0]->fused == 3 && G->m[0]->source == 0;
     for (int64_t step = 0; step < steps; ++step) {
-        for (int stage = 1; stage <= 3; ++stage) {
+        for (int kern = 1; kern <= (s12 ? 2 : 3); ++kern) {
             for (int r = 0; r < n; ++r) {
                 hsgn_ctx* c = G->m[r];
                 cudaSetDevice(c->device);
-                if (stage == 1) reset_recs(c, 1);
+                if (kern == 1) reset_recs(c, 1);
                 group_wait_pulls(G, r);
-                hsgn_status s = enqueue_stage(c, stage, Y[p][r], K[p][r], K2[r], Y[p ^ 1][r], K[p ^ 1][r], nullptr,
-                                              &c->d_rec[0], nullptr, t, dt, false, 0, 0);
+                hsgn_status s;
+                if (s12)
+                    s = kern == 1 ? enqueue_s12(c, Y[p][r], K[p][r], Y[p ^ 1][r], &c->d_rec[0], nullptr, dt)
+                                  : enqueue_s3_fixed(c, Y[p ^ 1][r], K[p ^ 1][r], &c->d_rec[0], dt);
+                else
+                    s = enqueue_stage(c, kern, Y[p][r], K[p][r], K2[r], Y[p ^ 1][r], K[p ^ 1][r], nullptr,
+                                      &c->d_rec[0], nullptr, t, dt, false, 0, 0);
                 if (s) return s;
                 cudaEventRecord(G->evk[r], c->stream);
             }
-            const std::vector<hsgn_state*>& produced = stage == 1 ? K2 : (stage == 2 ? Y[p ^ 1] : K[p ^ 1]);
+            const std::vector<hsgn_state*>& produced =
+                s12 ? (kern == 1 ? Y[p ^ 1] : K[p ^ 1]) : (kern == 1 ? K2 : (kern == 2 ? Y[p ^ 1] : K[p ^ 1]));
             hsgn_status s = group_pull(G, produced, 5);
             if (s) return s;
         }
@@ -2096,9 +2128,9 @@ hsgn_status hsgn_group_bs3_fixed_steps(hsgn_group* G, hsgn_gstate* y, hsgn_gstat
     for (int r = 0; r < n; ++r) {
         hsgn_ctx* c = G->m[r];
         cudaSetDevice(c->device);
-        cudaMemcpyAsync(y->p[r]->base - c->grid.nx, Y[p][r]->base - c->grid.nx, sizeof(double) * 5 * c->fs,
+        cudaMemcpyAsync(y->p[r]->base - GHOST * c->grid.nx, Y[p][r]->base - GHOST * c->grid.nx, sizeof(double) * 5 * c->fs,
                         cudaMemcpyDeviceToDevice, c->stream);
-        cudaMemcpyAsync(k1->p[r]->base - c->grid.nx, K[p][r]->base - c->grid.nx, sizeof(double) * 5 * c->fs,
+        cudaMemcpyAsync(k1->p[r]->base - GHOST * c->grid.nx, K[p][r]->base - GHOST * c->grid.nx, sizeof(double) * 5 * c->fs,
                         cudaMemcpyDeviceToDevice, c->stream);
         cudaStreamSynchronize(c->stream);
     }

@@ -79,9 +79,10 @@ struct YQ {  // y-differentiated quantities of one row at this column (rhs.hpp:1
     double h, u, v, w, e, hhb, v2, hv, huv, e2h, hvw, b;
 };
 
-// Memory row of logical row jr (may be -1 or ny) of the slab, counted from
-// the ghost row -1 (every KPtrs base points at row -1, so offsets stay
-// non-negative 32-bit values even for the lower ghost row).
+// Per-stage kernels: memory row of logical row jr (-1 <= jr <= ny) of the
+// slab counted from the ghost row -1 (their KPtrs bases point at row -1, so
+// offsets stay non-negative 32-bit values): wrap (periodic, whole grid),
+// clamp (wall) or the nearest ghost row (slab edge).
 __device__ __forceinline__ int map_row(const StageArgs& A, int jr) {
     if (jr < 0) return A.y_lo == YE_WRAP ? A.ny : (A.y_lo == YE_CLAMP ? 1 : 0);
     if (jr >= A.ny) return A.y_hi == YE_WRAP ? 1 : (A.y_hi == YE_CLAMP ? A.ny : A.ny + 1);
@@ -752,10 +753,12 @@ __global__ void __launch_bounds__(BX, min_blocks<MODE>()) sgn_stage_kernel(const
 constexpr int WX2 = BX - 4;
 constexpr int NPF = 4;  // ring pairs of the fused kernel (no P_RH)
 
+// Fused kernels: the same for -GHOST <= jr < ny + GHOST, counted from row
+// -GHOST (their KPtrs bases point there).
 __device__ __forceinline__ int map_row2(const StageArgs& A, int jr) {
-    if (jr < 0) return A.y_lo == YE_WRAP ? jr + A.ny + 1 : 1;
-    if (jr >= A.ny) return A.y_hi == YE_WRAP ? jr - A.ny + 1 : A.ny;
-    return jr + 1;
+    if (jr < 0) return A.y_lo == YE_WRAP ? jr + A.ny + GHOST : (A.y_lo == YE_CLAMP ? GHOST : jr + GHOST);
+    if (jr >= A.ny) return A.y_hi == YE_WRAP ? jr - A.ny + GHOST : (A.y_hi == YE_CLAMP ? A.ny - 1 + GHOST : jr + GHOST);
+    return jr + GHOST;
 }
 
 struct Thr2 {
@@ -785,7 +788,7 @@ __device__ __forceinline__ void s31_half3(const StageArgs& A, const KPtrs& P, Th
     tendency<KIND>(A, ac, T.tid, T.sl, T.sr, T.cx, cy, T.xl, T.xr, T.i, r, yp, yn, rh, o);
     const bool own = T.fb && r >= T.j0 && r < T.j1;
     if (own) {
-        const unsigned off = (unsigned)(r + 1) * (unsigned)A.nx + T.col;
+        const unsigned off = (unsigned)(r + GHOST) * (unsigned)A.nx + T.col;
 #pragma unroll
         for (int f = 0; f < 5; ++f) P.out[f][off] = o[f];
     }
@@ -822,7 +825,7 @@ __device__ __forceinline__ void s31_half1(const StageArgs& A, const KPtrs& P, co
     const double cy = (j == T.jc0 || j == T.jc1) ? A.c1y : A.cpy;
     double o[5];
     tendency<KIND>(A, bc, T.tid, T.sl, T.sr, T.cx, cy, T.xl, T.xr, T.i, j, yp, yn, rh, o);
-    const unsigned off = (unsigned)(j + 1) * (unsigned)A.nx + T.col;
+    const unsigned off = (unsigned)(j + GHOST) * (unsigned)A.nx + T.col;
 #pragma unroll
     for (int f = 0; f < 5; ++f) P.out2[f][off] = o[f];
 }
@@ -1073,7 +1076,7 @@ __global__ void __launch_bounds__(BX, HSGN_S12_MINB) sgn_s12_kernel(const StageA
             const double cy = (j == jc0 || j == jc1) ? A.c1y : A.cpy;
             double k3[5];
             tendency<KIND>(A, qb, tid, sl, sr, cx, cy, xl, xr, i, j, yp, hi ? yc : yb, rhbp, k3);
-            const unsigned off = (unsigned)(j + 1) * unx + col;
+            const unsigned off = (unsigned)(j + GHOST) * unx + col;
 #pragma unroll
             for (int f = 0; f < 5; ++f) P.out[f][off] = dadd(partp[f], dmul(A.c3, k3[f]));  // state_add3
             const unsigned long long bits =
@@ -1241,7 +1244,7 @@ __global__ void __launch_bounds__(BX, HSGN_STEP_MINB) sgn_step_kernel(const Stag
             for (int f = 0; f < 5; ++f) ynw[f] = dadd(partp[f], dmul(A.c3, k3[f]));  // state_add3
             const bool own = f3 && j >= j0 && j < j1;
             if (own) {
-                const unsigned off = (unsigned)(j + 1) * unx + col;
+                const unsigned off = (unsigned)(j + GHOST) * unx + col;
 #pragma unroll
                 for (int f = 0; f < 5; ++f) P.out[f][off] = ynw[f];
                 const unsigned long long bits = (unsigned long long)__double_as_longlong(ynw[0]);
@@ -1261,7 +1264,7 @@ __global__ void __launch_bounds__(BX, HSGN_STEP_MINB) sgn_step_kernel(const Stag
             const double cy = (j == jc0 || j == jc1) ? A.c1y : A.cpy;
             double k4[5];
             tendency<KIND>(A, p3b, tid, sl, sr, cx, cy, xl, xr, i, j, yp, hi ? yc : y3, rh3p, k4);
-            const unsigned off = (unsigned)(j + 1) * unx + col;
+            const unsigned off = (unsigned)(j + GHOST) * unx + col;
 #pragma unroll
             for (int f = 0; f < 5; ++f) P.out2[f][off] = k4[f];
         }
@@ -1367,7 +1370,7 @@ static cudaError_t launch_mode(const StageArgs& A, cudaStream_t st) {
         P.yold[f] = A.yold ? A.yold + f * A.fs - g : nullptr;
         P.out2[f] = A.out2 ? A.out2 + f * A.fs - g : nullptr;
     }
-    P.b = A.b - g;
+    P.b = A.b - g;  // per-stage kernels: bases at row -1 (see map_row)
     // TMA staging needs 16-byte aligned row pieces: nx even (host decides)
     if (A.tma && (A.nx % 2) == 0) return launch_tma<MODE, KIND, true>(A, P, st);
     return launch_tma<MODE, KIND, false>(A, P, st);
@@ -1386,13 +1389,13 @@ static cudaError_t launch_s31(const StageArgs& A, cudaStream_t st) {
     KPtrs P;
     const long long g = A.nx;
     for (int f = 0; f < 5; ++f) {
-        P.y[f] = A.y + f * A.fs - g;
+        P.y[f] = A.y + f * A.fs - GHOST * g;
         P.k[f] = P.kc[f] = P.yold[f] = nullptr;
         P.part[f] = nullptr;
-        P.out[f] = A.out + f * A.fs - g;
-        P.out2[f] = A.out2 + f * A.fs - g;
+        P.out[f] = A.out + f * A.fs - GHOST * g;
+        P.out2[f] = A.out2 + f * A.fs - GHOST * g;
     }
-    P.b = A.b - g;
+    P.b = A.b - GHOST * g;
     dim3 grid((A.nx + WX2 - 1) / WX2, (band_rows(A) + A.rows_per_block - 1) / A.rows_per_block);
     sgn_s31_kernel<KIND><<<grid, BX, bytes, st>>>(A, P);
     return cudaGetLastError();
@@ -1411,14 +1414,14 @@ static cudaError_t launch_step(const StageArgs& A, cudaStream_t st) {
     KPtrs P;
     const long long g = A.nx;
     for (int f = 0; f < 5; ++f) {
-        P.y[f] = A.y + f * A.fs - g;
-        P.k[f] = A.k + f * A.fs - g;
+        P.y[f] = A.y + f * A.fs - GHOST * g;
+        P.k[f] = A.k + f * A.fs - GHOST * g;
         P.kc[f] = P.yold[f] = nullptr;
         P.part[f] = nullptr;
-        P.out[f] = A.out + f * A.fs - g;
-        P.out2[f] = A.out2 + f * A.fs - g;
+        P.out[f] = A.out + f * A.fs - GHOST * g;
+        P.out2[f] = A.out2 + f * A.fs - GHOST * g;
     }
-    P.b = A.b - g;
+    P.b = A.b - GHOST * g;
     dim3 grid((A.nx + WX3 - 1) / WX3, (band_rows(A) + A.rows_per_block - 1) / A.rows_per_block);
     sgn_step_kernel<KIND><<<grid, BX, bytes, st>>>(A, P);
     return cudaGetLastError();
@@ -1437,13 +1440,13 @@ static cudaError_t launch_s12(const StageArgs& A, cudaStream_t st) {
     KPtrs P;
     const long long g = A.nx;
     for (int f = 0; f < 5; ++f) {
-        P.y[f] = A.y + f * A.fs - g;
-        P.k[f] = A.k + f * A.fs - g;
+        P.y[f] = A.y + f * A.fs - GHOST * g;
+        P.k[f] = A.k + f * A.fs - GHOST * g;
         P.kc[f] = P.yold[f] = nullptr;
         P.part[f] = P.out2[f] = nullptr;
-        P.out[f] = A.out + f * A.fs - g;
+        P.out[f] = A.out + f * A.fs - GHOST * g;
     }
-    P.b = A.b - g;
+    P.b = A.b - GHOST * g;
     dim3 grid((A.nx + WX2 - 1) / WX2, (band_rows(A) + A.rows_per_block - 1) / A.rows_per_block);
     sgn_s12_kernel<KIND><<<grid, BX, bytes, st>>>(A, P);
     return cudaGetLastError();

@@ -1,12 +1,14 @@
 """Slab domain decomposition over the GPUs of one box.
 
-The grid is cut into y-slabs of contiguous rows (x fastest, so a halo row is
-one contiguous nx*8 B span per field).  Each rank keeps one ghost row above
-and below its slab; after every stage the library exchanges the freshly
+The grid is cut into y-slabs of contiguous rows (x fastest, so the halo
+rows are one contiguous span per field).  Each rank keeps two ghost rows
+above and below its slab (the fused stage-1+2 kernel reads two rows beyond
+the rows it finishes); after every kernel the library exchanges the freshly
 written boundary rows with the two neighbours (ring wrap when y is
 periodic) through NCCL send/recv on its own stream.  Because ghost values
 are formed by the same expressions as interior ones, the P-rank state is
-bitwise equal to the 1-rank state (the RHS has no reductions).
+bitwise equal to the 1-rank state (the RHS has no reductions).  The
+host-side reference below exchanges one row (what a single stage needs).
 
 torch.distributed is the plumbing only: it carries the ncclUniqueId from
 rank 0 to the others and provides barriers / the max-over-ranks timing.
