@@ -1,10 +1,11 @@
 """Multi-rank slab decomposition on CPU (gloo, world_size 2 and 3).
 
 The library's multi-GPU path (hsgn_ctx_create_slab + NCCL halo exchange,
-hsgn_host.cu exchange()/enqueue_step()) cuts the grid into y-slabs with one
-ghost row above and below, and after every stage exchanges the rows just
-written: k2 after stage 1, ynew after stage 2, k4 after stage 3.  These tests
-run exactly that schedule with torch.distributed/gloo as the transport and
+hsgn_host.cu exchange()) cuts the grid into y-slabs with ghost rows above
+and below and exchanges the rows just written after every kernel: per stage
+(k2, ynew, k4; one row needed) or, with the default fused structure, ynew
+after S12 and k4 after S3 (two rows).  These tests run both schedules with
+torch.distributed/gloo as the transport and
 the CPU oracle as the stage arithmetic, and require the gathered P-rank
 state to be BIT-IDENTICAL to the single-domain reference solve (the RHS has
 no reductions, so decomposition must not change a single bit).
@@ -68,7 +69,7 @@ def _exchange_fn(rank, nranks, periodic_y):
     return exchange
 
 
-def _worker(rank, nranks, port, kind_y, steps, q_shared, result):
+def _worker(rank, nranks, port, kind_y, steps, q_shared, result, schedule="stage"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=nranks)
@@ -127,7 +128,47 @@ def _worker(rank, nranks, port, kind_y, steps, q_shared, result):
         y = q0[:, j0:j1].copy()
         dt = 0.25 * dx / 20.0
         k1 = rhs_slab(ghosted(y))
-        for _ in range(steps):
+
+        # ---- the default fixed-step structure S12 + S3:
+        # two ghost rows per side, halos of ynew after S12 and of k4 after S3
+        lo2, hi2 = (2 if dn >= 0 else 0), (2 if up >= 0 else 0)
+        wall_kind = 1 if (kind_y and (dn < 0 or up < 0)) else 0
+
+        def ext2(field):  # (n_loc, nx) -> two exchanged ghost rows on each interior side
+            fb, fa = exch(field[:2].ravel().copy() if dn >= 0 else None,
+                          field[-2:].ravel().copy() if up >= 0 else None)
+            parts = ([fb.reshape(2, nx)] if dn >= 0 else []) + [field] + ([fa.reshape(2, nx)] if up >= 0 else [])
+            return np.concatenate(parts, axis=0)
+
+        def ext2_state(qs):
+            return np.stack([ext2(qs[f]) for f in range(5)])
+
+        def rhs_rows(arr, bb):  # tendencies of every row of an extended array (edges invalid)
+            rows = arr.shape[1]
+            gg = omake(nx, rows, kind_x=0, kind_y=wall_kind)
+            out = np.empty(5 * rows * nx)
+            assert orc._lib_rhs_dxdy(gg, dx, dy, ph, np.ascontiguousarray(bb).ravel(),
+                                     np.ascontiguousarray(arr).ravel(), out) == 0
+            return out.reshape(5, rows, nx)
+
+        b2 = ext2(b[j0:j1])
+        if schedule == "s12":
+            y_e, k1_e = ext2_state(y), ext2_state(k1)
+            for _ in range(steps):
+                k2_e = rhs_rows(y_e + (0.5 * dt) * k1_e, b2)           # S12: stage 1 on slab rows -1..n
+                s0, s1 = (1 if dn >= 0 else 0), y_e.shape[1] - (1 if up >= 0 else 0)
+                q2 = (y_e + (0.75 * dt) * k2_e)[:, s0:s1]              # stage-2 input, rows -1..n
+                k3 = rhs_rows(q2, b2[s0:s1])[:, lo2 - s0:lo2 - s0 + n_loc]
+                yy, kk1, kk2 = y_e[:, lo2:lo2 + n_loc], k1_e[:, lo2:lo2 + n_loc], k2_e[:, lo2:lo2 + n_loc]
+                ynew = yy + (dt * (2.0 / 9.0)) * kk1 + (dt * (1.0 / 3.0)) * kk2 + (dt * (4.0 / 9.0)) * k3
+                y_e = ext2_state(ynew)                                  # ynew halo (2 rows)
+                k4 = rhs_rows(y_e, b2)[:, lo2:lo2 + n_loc]              # S3
+                k1_e = ext2_state(k4)                                   # k4 halo (2 rows)
+            y = y_e[:, lo2:lo2 + n_loc]
+            steps_left = 0
+        else:
+            steps_left = steps
+        for _ in range(steps_left):
             yg, k1g = ghosted(y), ghosted(k1)
             k2 = rhs_slab(yg + (0.5 * dt) * k1g)                    # stage 1 (then k2 halo)
             k2g = ghosted(k2)
@@ -167,8 +208,12 @@ def _oracle_lib_patch():
     Oracle._lib_rhs_dxdy = rhs_dxdy
 
 
+@pytest.mark.parametrize("schedule", ["stage", "s12"])
 @pytest.mark.parametrize("nranks,kind_y", [(2, 0), (3, 0), (2, 1), (3, 1)])
-def test_slab_bs3_bitwise_equals_single_domain(nranks, kind_y):
+def test_slab_bs3_bitwise_equals_single_domain(nranks, kind_y, schedule):
+    """schedule "stage": one ghost row, halos after every stage (the
+    per-stage kernels); "s12": two ghost rows, halos of ynew after S12 and
+    of k4 after S3 (the default fused structure)."""
     import sys
     sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
     from oracle_lib import Oracle, Phys, default_cfg, make_grid as omake, mms_exact_field
@@ -193,7 +238,8 @@ def test_slab_bs3_bitwise_equals_single_domain(nranks, kind_y):
     q_shared = (ctx.RawArray("b", q0.tobytes()), ctx.RawArray("b", b.tobytes()))
     result = ctx.Queue()
     port = free_port()
-    procs = [ctx.Process(target=_worker_entry, args=(r, nranks, port, kind_y, rec.accepted, q_shared, result))
+    procs = [ctx.Process(target=_worker_entry,
+                         args=(r, nranks, port, kind_y, rec.accepted, q_shared, result, schedule))
              for r in range(nranks)]
     for p in procs:
         p.start()
