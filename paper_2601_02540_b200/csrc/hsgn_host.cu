@@ -528,7 +528,7 @@ static hsgn_status enqueue_chunk_step(hsgn_ctx* c, int parity, int steps, double
 // each followed by the slab halo exchange of its output (no-op on a whole
 // grid; in an in-process group the driver pulls instead: pass `group`).
 static hsgn_status enqueue_s12(hsgn_ctx* c, const hsgn_state* y, const hsgn_state* k1, hsgn_state* ynew,
-                               StepRec* rec, const StepRec* prev, double dt) {
+                               StepRec* rec, const StepRec* prev, double dt, hsgn_state* part = nullptr) {
     StageArgs A = stage_args(c, MODE_S12, 0.0);
     A.a = 0.5 * dt;
     A.a2 = 0.75 * dt;
@@ -544,6 +544,13 @@ static hsgn_status enqueue_s12(hsgn_ctx* c, const hsgn_state* y, const hsgn_stat
     A.halt = c->d_halt;
     A.chk_bad = prev ? &prev->bad[2] : nullptr;
     A.chk_minh = prev ? &prev->minh : nullptr;
+    if (part) {  // adaptive attempt: error partials for the adaptive S3
+        A.adaptive = 1;
+        A.d1 = -5.0 / 72.0;
+        A.d2 = 1.0 / 12.0;
+        A.d3 = 1.0 / 9.0;
+        A.part = part->base;
+    }
     return launch(c, MODE_S12, A);
 }
 
@@ -1435,8 +1442,19 @@ extern "C" hsgn_status hsgn_solve_recorded(hsgn_ctx* c, const hsgn_state* q0, do
         // ---- one attempt (adaptive, clipped or observed step)
         const int q = p ^ 1;
         reset_recs(c, 1);
-        st = enqueue_step(c, &c->ws[p], &c->ws[2 + p], &c->ws[4], &c->ws[q], &c->ws[2 + q], &c->ws[5],
-                          &c->d_rec[0], nullptr, t, dt, !fixed, cfg->abs_tol, cfg->rel_tol, &kernels);
+        if (c->fused == 3 && c->source == 0) {  // S12 + S3 (with error partials when adaptive)
+            st = enqueue_s12(c, &c->ws[p], &c->ws[2 + p], &c->ws[q], &c->d_rec[0], nullptr, dt,
+                             fixed ? nullptr : &c->ws[5]);
+            if (!st) st = exchange(c, &c->ws[q], 5);
+            if (!st)
+                st = enqueue_stage(c, 3, &c->ws[p], &c->ws[2 + p], &c->ws[4], &c->ws[q], &c->ws[2 + q], &c->ws[5],
+                                   &c->d_rec[0], nullptr, t, dt, !fixed, cfg->abs_tol, cfg->rel_tol);
+            if (!st) st = exchange(c, &c->ws[2 + q], 5);
+            kernels += 2;
+        } else {
+            st = enqueue_step(c, &c->ws[p], &c->ws[2 + p], &c->ws[4], &c->ws[q], &c->ws[2 + q], &c->ws[5],
+                              &c->d_rec[0], nullptr, t, dt, !fixed, cfg->abs_tol, cfg->rel_tol, &kernels);
+        }
         if (st) return st;
         if (!fixed) CK(launch_sum_partials(c->d_err_part, stage_grid_blocks(c->base), c->d_scalar, c->stream));
         StepRec r;

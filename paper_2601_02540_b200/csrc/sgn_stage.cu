@@ -52,7 +52,7 @@ __host__ __device__ constexpr int min_blocks() {
     // measured (r1): S2 (largest ring, 16 raw inputs) is best at 3 CTAs/SM;
     // the other stages fit 96 registers without spills and run best at 5
     // (expressed as resident warps per SM: 12 for S2, 20 for the others)
-    return HSGN_MIN_BLOCKS > 0 ? HSGN_MIN_BLOCKS : (MODE == MODE_S2 ? 12 : 20) / (BX / 32);
+    return HSGN_MIN_BLOCKS > 0 ? HSGN_MIN_BLOCKS : (MODE == MODE_S2 ? 12 : MODE == MODE_S3A ? 16 : 20) / (BX / 32);
 }
 
 // Per-field device pointers (kernel parameters live in the constant bank, so
@@ -214,24 +214,6 @@ __device__ __noinline__ void s2_error_partial(const double* kc, const double* k,
         part[f * fs + off] = dadd(dadd(dmul(d1, k1v), dmul(d2, k2v)), dmul(d3, o[f]));
     }
 }
-// S3: sum_f (e_f / scale_f)^2 at one node (time_integration.hpp:127-136)
-__device__ __noinline__ double s3_error_sq(const double* part, const double* yold, const double* ynew, long long fs,
-                                           unsigned off, double dt, double d4, double atol, double rtol, double o0,
-                                           double o1, double o2, double o3, double o4) {
-    const double o[5] = {o0, o1, o2, o3, o4};
-    double acc = 0.0;
-#pragma unroll
-    for (int f = 0; f < 5; ++f) {
-        const double e = dmul(dt, dadd(part[f * fs + off], dmul(d4, o[f])));
-        const double ay = fabs(__ldg(yold + f * fs + off));
-        const double an = fabs(__ldg(ynew + f * fs + off));
-        const double scale = dadd(atol, dmul(rtol, ay < an ? an : ay));
-        const double rq = e / scale;
-        acc = dadd(acc, dmul(rq, rq));
-    }
-    return acc;
-}
-
 __device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -563,10 +545,20 @@ __device__ __forceinline__ void march_row(const StageArgs& A, const KPtrs& P, Th
     YQ yprev;
     if (ywin_smem) neighbour_y(ring + ((SC + 2) % 3) * (NP * BX) + T.tid, yprev);
     const YQ& ypr = ywin_smem ? yprev : yp;
+    const unsigned off = (unsigned)(j + 1) * nx + T.col;  // bases point at row -1
+    // S3A: the error-norm inputs of this node are requested before the
+    // tendency so their latency hides behind it
+    double e_part[5], e_yold[5];
+    if (MODE == MODE_S3A) {
+#pragma unroll
+        for (int f = 0; f < 5; ++f) {
+            e_part[f] = P.part[f][off];
+            e_yold[f] = __ldg(P.yold[f] + off);
+        }
+    }
     double o[5];
     tendency<KIND>(A, S, T.tid, T.sl, T.sr, T.cx, cy, T.xl, T.xr, T.i, j, ypr, yn, Sc[P_RH * BX].x, o);
     // ---- epilogue
-    const unsigned off = (unsigned)(j + 1) * nx + T.col;  // bases point at row -1
     if (MODE == MODE_S2) {
         const double2 y01 = Sc[P_YP01 * BX], y23 = Sc[P_YP23 * BX], y4 = Sc[P_YP4 * BX];
         const double ypart[5] = {y01.x, y01.y, y23.x, y23.y, y4.x};
@@ -585,10 +577,20 @@ __device__ __forceinline__ void march_row(const StageArgs& A, const KPtrs& P, Th
     } else {
 #pragma unroll
         for (int f = 0; f < 5; ++f) P.out[f][off] = o[f];
-        if (MODE == MODE_S3 && A.adaptive)
-            T.my_err = dadd(T.my_err, s3_error_sq(A.part - A.nx, A.yold - A.nx, A.y - A.nx, A.fs, off, A.dt, A.d4,
-                                                  A.atol, A.rtol, o[0],
-                                                  o[1], o[2], o[3], o[4]));
+        if (MODE == MODE_S3A) {  // sum_f (e_f / scale_f)^2 (time_integration.hpp:127-136)
+            const double2 c0 = Sc[P_HU * BX], c1 = Sc[P_VW * BX], c2 = Sc[P_EB * BX];
+            const double yn5[5] = {c0.x, c0.y, c1.x, c1.y, c2.x};  // ynew = this stage's input
+            double acc = 0.0;
+#pragma unroll
+            for (int f = 0; f < 5; ++f) {
+                const double e = dmul(A.dt, dadd(e_part[f], dmul(A.d4, o[f])));
+                const double ay = fabs(e_yold[f]), an = fabs(yn5[f]);
+                const double scale = dadd(A.atol, dmul(A.rtol, ay < an ? an : ay));
+                const double rq = e / scale;
+                acc = dadd(acc, dmul(rq, rq));
+            }
+            T.my_err = dadd(T.my_err, acc);
+        }
     }
 }
 
@@ -720,7 +722,7 @@ __global__ void __launch_bounds__(BX, min_blocks<MODE>()) sgn_stage_kernel(const
             if (mm != ~0ull) atomicMin(A.minh, mm);
         }
     }
-    if (MODE == MODE_S3 && A.adaptive) {
+    if (MODE == MODE_S3A) {
         const double s = warp_sum(T.my_err);
         if (lane == 0) s_err[warp] = s;
         __syncthreads();
@@ -974,7 +976,10 @@ __device__ __forceinline__ void ywin_prev(const StageArgs& A, int j, const doubl
 #define HSGN_S12_LATE_PF 0
 #endif
 
-template <int KIND>
+// ADAPT: also store the error partial ((d1 k1 + d2 k2) + d3 k3)
+// (time_integration.hpp:128-129, the S2 epilogue of the per-stage path) for
+// the adaptive S3's error norm.
+template <int KIND, bool ADAPT>
 __global__ void __launch_bounds__(BX, HSGN_S12_MINB) sgn_s12_kernel(const StageArgs A, const KPtrs P) {
     extern __shared__ __align__(16) double2 ring[];  // ring A | ring B, each 3 x NPF x BX
     __shared__ unsigned long long s_min[BX / 32];
@@ -1062,6 +1067,11 @@ __global__ void __launch_bounds__(BX, HSGN_S12_MINB) sgn_s12_kernel(const StageA
                 q[f] = dadd(yj[f], dmul(A.a2, k2[f]));                                  // state_add1
                 partc[f] = dadd(dadd(yj[f], dmul(A.c1, kj[f])), dmul(A.c2, k2[f]));  // state_add3, 2 terms
             }
+            if (ADAPT && fb && j >= j0 && j < j1) {  // d1 k1 + d2 k2 of row j, completed by H2 one row later
+                const unsigned offe = (unsigned)(j + GHOST) * unx + col;
+#pragma unroll
+                for (int f = 0; f < 5; ++f) P.part[f][offe] = dadd(dmul(A.d1, kj[f]), dmul(A.d2, k2[f]));
+            }
             const bool ok = products_q<false>(q, pb[tid + P_EB * BX].y, qc + tid, yb, &rhbc);
             if (fb && j >= j0 && j < j1 && !ok) ++bad2;
         }
@@ -1074,11 +1084,20 @@ __global__ void __launch_bounds__(BX, HSGN_S12_MINB) sgn_s12_kernel(const StageA
             const bool hi = clamp_hi && j == ny - 1;
             if (hi) neighbour_y(qb + tid, yc);
             const double cy = (j == jc0 || j == jc1) ? A.c1y : A.cpy;
+            const unsigned off = (unsigned)(j + GHOST) * unx + col;
+            double e12[5];  // ADAPT: d1 k1 + d2 k2 stored by H1 one row ago (requested before the tendency)
+            if (ADAPT) {
+#pragma unroll
+                for (int f = 0; f < 5; ++f) e12[f] = P.part[f][off];
+            }
             double k3[5];
             tendency<KIND>(A, qb, tid, sl, sr, cx, cy, xl, xr, i, j, yp, hi ? yc : yb, rhbp, k3);
-            const unsigned off = (unsigned)(j + GHOST) * unx + col;
 #pragma unroll
             for (int f = 0; f < 5; ++f) P.out[f][off] = dadd(partp[f], dmul(A.c3, k3[f]));  // state_add3
+            if (ADAPT) {  // ((d1 k1 + d2 k2) + d3 k3) (time_integration.hpp:128-129)
+#pragma unroll
+                for (int f = 0; f < 5; ++f) P.part[f][off] = dadd(e12[f], dmul(A.d3, k3[f]));
+            }
             const unsigned long long bits =
                 (unsigned long long)__double_as_longlong(dadd(partp[0], dmul(A.c3, k3[0])));
             my_min = bits < my_min ? bits : my_min;
@@ -1433,7 +1452,10 @@ static cudaError_t launch_s12(const StageArgs& A, cudaStream_t st) {
     static bool configured = false;
     if (!configured) {
         cudaError_t e =
-            cudaFuncSetAttribute(sgn_s12_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+            cudaFuncSetAttribute(sgn_s12_kernel<KIND, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(sgn_s12_kernel<KIND, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)bytes);
         if (e != cudaSuccess) return e;
         configured = true;
     }
@@ -1443,12 +1465,16 @@ static cudaError_t launch_s12(const StageArgs& A, cudaStream_t st) {
         P.y[f] = A.y + f * A.fs - GHOST * g;
         P.k[f] = A.k + f * A.fs - GHOST * g;
         P.kc[f] = P.yold[f] = nullptr;
-        P.part[f] = P.out2[f] = nullptr;
+        P.out2[f] = nullptr;
+        P.part[f] = A.part ? A.part + f * A.fs - GHOST * g : nullptr;
         P.out[f] = A.out + f * A.fs - GHOST * g;
     }
     P.b = A.b - GHOST * g;
     dim3 grid((A.nx + WX2 - 1) / WX2, (band_rows(A) + A.rows_per_block - 1) / A.rows_per_block);
-    sgn_s12_kernel<KIND><<<grid, BX, bytes, st>>>(A, P);
+    if (A.adaptive)
+        sgn_s12_kernel<KIND, true><<<grid, BX, bytes, st>>>(A, P);
+    else
+        sgn_s12_kernel<KIND, false><<<grid, BX, bytes, st>>>(A, P);
     return cudaGetLastError();
 }
 
@@ -1461,7 +1487,7 @@ static cudaError_t launch_kind(int mode, const StageArgs& A, cudaStream_t st) {
         case MODE_RHS: return launch_mode<MODE_RHS, KIND>(A, st);
         case MODE_S1: return launch_mode<MODE_S1, KIND>(A, st);
         case MODE_S2: return launch_mode<MODE_S2, KIND>(A, st);
-        default: return launch_mode<MODE_S3, KIND>(A, st);
+        default: return A.adaptive ? launch_mode<MODE_S3A, KIND>(A, st) : launch_mode<MODE_S3, KIND>(A, st);
     }
 }
 

@@ -126,3 +126,23 @@ def test_fused_structures_deterministic_under_repetition(kind):
             if first is None:
                 first = flat
             assert _neq(flat, first) == 0, (rep, mode)
+
+
+@pytest.mark.parametrize("kind", [0, 1])
+def test_adaptive_attempts_fused_equal_unfused(kind):
+    """Adaptive attempts run S12 (with the error partials) + S3 in mode 3:
+    the error norms, hence the step sequence and the state, must equal the
+    per-stage path bit for bit."""
+    nx, ny = 96, 80
+    og = omake_grid(nx, ny, kind_x=kind, kind_y=kind)
+    q, b = mms_exact_field(og, 0.3)
+    g, ctx = _ctx(og, b)
+    res = {}
+    for mode in (0, 3):
+        ctx.fused_stages = mode
+        r = H.adaptive_solve(ctx, H.StateField(g, q), 0.0, 0.02, H.IntegratorConfig(abs_tol=1e-8, rel_tol=1e-8))
+        assert not r.aborted
+        res[mode] = r
+    assert (res[0].accepted, res[0].rejected, res[0].t) == (res[3].accepted, res[3].rejected, res[3].t)
+    assert res[0].accepted > 3
+    assert _neq(res[0].q.flat(), res[3].q.flat()) == 0
