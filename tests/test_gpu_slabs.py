@@ -14,9 +14,12 @@ from paper_2601_02540_b200 import slab as S  # noqa: E402
 from paper_2601_02540_b200.workloads import mms_fields  # noqa: E402
 
 
-@pytest.mark.parametrize("n,kind_y", [(2, 0), (3, 0), (4, 1), (3, 1), (5, 0)])
-def test_group_matches_single_context_bitwise(n, kind_y):
-    nx, ny = 96, 70
+@pytest.mark.parametrize("n,kind_y,ny", [(2, 0, 70), (3, 0, 70), (4, 1, 70), (3, 1, 70), (5, 0, 70),
+                                         (5, 0, 10), (5, 1, 10), (4, 0, 9)])
+def test_group_matches_single_context_bitwise(n, kind_y, ny):
+    """(ny = 10, 9 with 4-5 slabs: slabs of 2-3 rows, i.e. as thin as the two
+    ghost rows the fused S12 kernel reads across a slab edge.)"""
+    nx = 96
     g, q, b = mms_fields(nx, ny, 0.3, kind_y=H.BoundaryKind(kind_y))
     phys = H.PhysSetup(9.81, 500.0, 1e-12, b.reshape(ny, nx))
     ctx = H.make_rhs_context(g, phys)
