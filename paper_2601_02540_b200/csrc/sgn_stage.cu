@@ -1361,16 +1361,25 @@ __host__ __device__ constexpr size_t ring_bytes() {
     return sizeof(double2) * 3 * npairs<MODE>() * BX + (TMA ? sizeof(double) * RSLOTS * nraw<MODE>() * RW : 0);
 }
 
+// Dynamic shared memory above the 48 KB default needs a per-function opt-in,
+// and the attribute is per device: opt each kernel in once on every device
+// it is launched on (a racing second opt-in from another host thread is
+// harmless).
+template <class K>
+static cudaError_t smem_opt_in(unsigned long long& done, K kernel, size_t bytes) {
+    int d = 0;
+    cudaGetDevice(&d);
+    if (d < 64 && ((done >> d) & 1ull)) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess && d < 64) done |= 1ull << d;
+    return e;
+}
+
 template <int MODE, int KIND, bool TMA>
 static cudaError_t launch_tma(const StageArgs& A, const KPtrs& P, cudaStream_t st) {
-    static bool configured = false;  // one-time opt-in above the 48 KB default
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(sgn_stage_kernel<MODE, KIND, TMA>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)ring_bytes<MODE, TMA>());
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+    static unsigned long long opted = 0;
+    const cudaError_t e = smem_opt_in(opted, sgn_stage_kernel<MODE, KIND, TMA>, ring_bytes<MODE, TMA>());
+    if (e != cudaSuccess) return e;
     dim3 grid((A.nx + WX - 1) / WX, (band_rows(A) + A.rows_per_block - 1) / A.rows_per_block);
     sgn_stage_kernel<MODE, KIND, TMA><<<grid, BX, ring_bytes<MODE, TMA>(), st>>>(A, P);
     return cudaGetLastError();
@@ -1398,13 +1407,9 @@ static cudaError_t launch_mode(const StageArgs& A, cudaStream_t st) {
 template <int KIND>
 static cudaError_t launch_s31(const StageArgs& A, cudaStream_t st) {
     constexpr size_t bytes = sizeof(double2) * 2 * 3 * NPF * BX;
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e =
-            cudaFuncSetAttribute(sgn_s31_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+    static unsigned long long opted = 0;
+    const cudaError_t e = smem_opt_in(opted, sgn_s31_kernel<KIND>, bytes);
+    if (e != cudaSuccess) return e;
     KPtrs P;
     const long long g = A.nx;
     for (int f = 0; f < 5; ++f) {
@@ -1423,13 +1428,9 @@ static cudaError_t launch_s31(const StageArgs& A, cudaStream_t st) {
 template <int KIND>
 static cudaError_t launch_step(const StageArgs& A, cudaStream_t st) {
     constexpr size_t bytes = sizeof(double2) * 3 * 3 * NPF * BX;
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e =
-            cudaFuncSetAttribute(sgn_step_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+    static unsigned long long opted = 0;
+    const cudaError_t e = smem_opt_in(opted, sgn_step_kernel<KIND>, bytes);
+    if (e != cudaSuccess) return e;
     KPtrs P;
     const long long g = A.nx;
     for (int f = 0; f < 5; ++f) {
@@ -1449,16 +1450,10 @@ static cudaError_t launch_step(const StageArgs& A, cudaStream_t st) {
 template <int KIND>
 static cudaError_t launch_s12(const StageArgs& A, cudaStream_t st) {
     constexpr size_t bytes = sizeof(double2) * 2 * 3 * NPF * BX;
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e =
-            cudaFuncSetAttribute(sgn_s12_kernel<KIND, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(sgn_s12_kernel<KIND, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)bytes);
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+    static unsigned long long opted_f = 0, opted_a = 0;
+    cudaError_t e = smem_opt_in(opted_f, sgn_s12_kernel<KIND, false>, bytes);
+    if (e == cudaSuccess) e = smem_opt_in(opted_a, sgn_s12_kernel<KIND, true>, bytes);
+    if (e != cudaSuccess) return e;
     KPtrs P;
     const long long g = A.nx;
     for (int f = 0; f < 5; ++f) {
