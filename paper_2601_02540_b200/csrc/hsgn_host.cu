@@ -202,6 +202,30 @@ hsgn_status fail(hsgn_ctx* c, hsgn_status s, const char* fmt, ...) {
         if (e_ != cudaSuccess) return fail(c, HSGN_ECUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
     } while (0)
 
+// Every entry point runs on its context's device and leaves the caller's
+// current device as it found it (torch and other libraries rely on it).
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int d) {
+        int cur = -1;
+        if (cudaGetDevice(&cur) == cudaSuccess && cur == d) return;  // nothing to switch or restore
+        prev = cur;
+        cudaSetDevice(d);
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+struct DeviceRestore {  // the group functions switch devices per member
+    int prev = -1;
+    DeviceRestore() {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    }
+    ~DeviceRestore() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
 bool is_pow2_ge1(double v) {
     if (!(v >= 1.0) || !std::isfinite(v)) return false;
     int e;
@@ -708,6 +732,7 @@ static double outer_sum(const hsgn_grid* g, const double* rows, int j_begin, int
 
 static hsgn_status reduce_full(hsgn_ctx* c, int kind, const hsgn_state* q, const hsgn_state* qt, int field,
                                double* out) {
+    DeviceGuard dg_(c->device);
     if (c->nranks != 1)
         return fail(c, HSGN_EINVAL, "slab contexts reduce via hsgn_row_sums + hsgn_outer_sum");
     hsgn_status s = row_sums_dev(c, kind, q, qt, field);
@@ -726,6 +751,7 @@ const char* hsgn_build_info(void) {
 
 static hsgn_status create_common(const hsgn_grid* grid, const hsgn_phys* phys, const double* b_host, int device,
                                  int j_begin, int j_end, int rank, int nranks, hsgn_ctx** out) {
+    DeviceRestore dr_;
     if (!grid || !phys || !b_host || !out) return HSGN_EINVAL;
     *out = nullptr;
     hsgn_ctx* c = new hsgn_ctx();
@@ -804,7 +830,7 @@ hsgn_status hsgn_ctx_attach_nccl(hsgn_ctx* c, const unsigned char nccl_id[128]) 
     if (!N.ok) return fail(c, HSGN_ENCCL, "libnccl.so.2 not loadable");
     nccl_uid id;
     std::memcpy(id.internal, nccl_id, 128);
-    CK(cudaSetDevice(c->device));
+    DeviceGuard dg_(c->device);
     int r = N.init_rank(&c->comm, c->nranks, id, c->rank);
     if (r) return fail(c, HSGN_ENCCL, "ncclCommInitRank failed (%d)", r);
     // exchange b's ghost rows once (static field)
@@ -819,7 +845,7 @@ hsgn_status hsgn_ctx_attach_nccl(hsgn_ctx* c, const unsigned char nccl_id[128]) 
 
 hsgn_status hsgn_ctx_destroy(hsgn_ctx* c) {
     if (!c) return HSGN_OK;
-    cudaSetDevice(c->device);
+    DeviceGuard dg_(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
     for (auto& kv : c->graphs)
         if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
@@ -850,6 +876,7 @@ hsgn_status hsgn_set_source(hsgn_ctx* c, int32_t kind) {
 }
 
 static hsgn_status reconfigure(hsgn_ctx* c) {
+    DeviceGuard dg_(c->device);
     cudaStreamSynchronize(c->stream);
     setup_ctx(c);
     for (auto& kv : c->graphs)
@@ -900,7 +927,7 @@ int64_t hsgn_n_evals(const hsgn_ctx* c) { return c ? c->n_evals : 0; }
 
 hsgn_status hsgn_state_alloc(hsgn_ctx* c, hsgn_state** out) {
     if (!c || !out) return HSGN_EINVAL;
-    CK(cudaSetDevice(c->device));
+    DeviceGuard dg_(c->device);
     hsgn_state* s = new hsgn_state();
     hsgn_status st = alloc_state(c, s);
     if (st) {
@@ -914,6 +941,7 @@ hsgn_status hsgn_state_alloc(hsgn_ctx* c, hsgn_state** out) {
 
 hsgn_status hsgn_state_free(hsgn_ctx* c, hsgn_state* s) {
     if (!c || !s) return HSGN_EINVAL;
+    DeviceGuard dg_(c->device);
     cudaStreamSynchronize(c->stream);
     free_state_c(c, s);
     delete s;
@@ -922,6 +950,7 @@ hsgn_status hsgn_state_free(hsgn_ctx* c, hsgn_state* s) {
 
 hsgn_status hsgn_state_upload(hsgn_ctx* c, hsgn_state* s, const double* host) {
     if (!c || !s || !host) return HSGN_EINVAL;
+    DeviceGuard dg_(c->device);
     const long long n = (long long)c->ny_loc * c->grid.nx;
     for (int f = 0; f < 5; ++f)
         CK(cudaMemcpyAsync(s->f(f), host + f * n, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
@@ -933,6 +962,7 @@ hsgn_status hsgn_state_upload(hsgn_ctx* c, hsgn_state* s, const double* host) {
 
 hsgn_status hsgn_state_download(hsgn_ctx* c, const hsgn_state* s, double* host) {
     if (!c || !s || !host) return HSGN_EINVAL;
+    DeviceGuard dg_(c->device);
     const long long n = (long long)c->ny_loc * c->grid.nx;
     for (int f = 0; f < 5; ++f)
         CK(cudaMemcpyAsync(host + f * n, s->f(f), sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
@@ -942,6 +972,7 @@ hsgn_status hsgn_state_download(hsgn_ctx* c, const hsgn_state* s, double* host) 
 
 hsgn_status hsgn_state_copy(hsgn_ctx* c, const hsgn_state* src, hsgn_state* dst) {
     if (!c || !src || !dst) return HSGN_EINVAL;
+    DeviceGuard dg_(c->device);
     CK(cudaMemcpyAsync(dst->base - GHOST * c->grid.nx, src->base - GHOST * c->grid.nx, sizeof(double) * 5 * c->fs,
                        cudaMemcpyDeviceToDevice, c->stream));
     CK(cudaStreamSynchronize(c->stream));
@@ -956,20 +987,20 @@ hsgn_status hsgn_state_field_ptr(const hsgn_state* s, int32_t f, double** out) {
 
 hsgn_status hsgn_rhs(hsgn_ctx* c, double t, const hsgn_state* q, hsgn_state* out, int64_t* bad_nodes) {
     if (!c || !q || !out) return HSGN_EINVAL;
-    CK(cudaSetDevice(c->device));
+    DeviceGuard dg_(c->device);
     return rhs_checked(c, t, q, out, false, bad_nodes);
 }
 
 hsgn_status hsgn_rhs_shallow_water(hsgn_ctx* c, double t, const hsgn_state* q, hsgn_state* out,
                                    int64_t* bad_nodes) {
     if (!c || !q || !out) return HSGN_EINVAL;
-    CK(cudaSetDevice(c->device));
+    DeviceGuard dg_(c->device);
     return rhs_checked(c, t, q, out, true, bad_nodes);
 }
 
 hsgn_status hsgn_init_auxiliary(hsgn_ctx* c, hsgn_state* q) {
     if (!c || !q) return HSGN_EINVAL;
-    CK(cudaSetDevice(c->device));
+    DeviceGuard dg_(c->device);
     // u, v ghost rows must be current for the slab y-derivative
     hsgn_status s = exchange(c, q, 3);
     if (s) return s;
@@ -1009,6 +1040,7 @@ hsgn_status hsgn_discrete_l2_error(hsgn_ctx* c, const hsgn_state* a, const hsgn_
 hsgn_status hsgn_row_sums(hsgn_ctx* c, int32_t kind, const hsgn_state* q, const hsgn_state* qt, int32_t field,
                           double* rows_host) {
     if (!c || !q || !rows_host || kind < 0 || kind > 3) return HSGN_EINVAL;
+    DeviceGuard dg_(c->device);
     hsgn_status s = row_sums_dev(c, kind, q, qt, field);
     if (s) return s;
     std::memcpy(rows_host, c->h_rows, sizeof(double) * c->ny_loc);
@@ -1020,6 +1052,7 @@ double hsgn_outer_sum(const hsgn_grid* g, const double* rows, int32_t j_begin, i
 
 hsgn_status hsgn_synchronize(hsgn_ctx* c) {
     if (!c) return HSGN_EINVAL;
+    DeviceGuard dg_(c->device);
     CK(cudaStreamSynchronize(c->stream));
     return HSGN_OK;
 }
@@ -1269,7 +1302,7 @@ extern "C" hsgn_status hsgn_solve_recorded(hsgn_ctx* c, const hsgn_state* q0, do
                                            hsgn_observer obs, void* user, hsgn_recorder* R) {
     if (!c || !q0 || !cfg || !q_out || !rec) return HSGN_EINVAL;
     if (R && R->c != c) return fail(c, HSGN_EINVAL, "recorder belongs to another context");
-    CK(cudaSetDevice(c->device));
+    DeviceGuard dg_(c->device);
     std::memset(rec, 0, sizeof *rec);
     rec->t = t0;
     hsgn_status st;
@@ -1530,7 +1563,7 @@ extern "C" hsgn_status hsgn_recorder_create(hsgn_ctx* c, int32_t n_gauges, const
     if (conservation_stride < 1)  // config.hpp:234-237
         return fail(c, HSGN_EINVAL, "conservation_stride must be >= 1");
     if (c->nranks != 1) return fail(c, HSGN_EINVAL, "the recorder needs a whole-grid context");
-    CK(cudaSetDevice(c->device));
+    DeviceGuard dg_(c->device);
     hsgn_recorder* R = new hsgn_recorder;
     R->c = c;
     R->stride = conservation_stride;
@@ -1569,6 +1602,7 @@ extern "C" hsgn_status hsgn_recorder_create(hsgn_ctx* c, int32_t n_gauges, const
 
 extern "C" hsgn_status hsgn_recorder_destroy(hsgn_recorder* R) {
     if (!R) return HSGN_OK;
+    DeviceRestore dr_;
     if (R->c) cudaSetDevice(R->c->device);
     if (R->c) cudaStreamSynchronize(R->c->stream);  // pending snapshot copies
     cudaFree(R->d_idx);
@@ -1621,7 +1655,7 @@ extern "C" hsgn_status hsgn_recorder_snapshot(const hsgn_recorder* R, int32_t k,
     if (actual) *actual = s.actual;
     if (host_state) {
         hsgn_ctx* c = R->c;
-        CK(cudaSetDevice(c->device));
+        DeviceGuard dg_(c->device);
         CK(cudaStreamSynchronize(c->stream));  // the stream-ordered copy has landed
         std::memcpy(host_state, s.host, sizeof(double) * 5 * (size_t)c->grid.nx * c->ny_loc);
     }
@@ -1631,7 +1665,7 @@ extern "C" hsgn_status hsgn_recorder_snapshot(const hsgn_recorder* R, int32_t k,
 extern "C" hsgn_status hsgn_bs3_fixed_steps(hsgn_ctx* c, hsgn_state* y, hsgn_state* k1, double t, double dt,
                                             int64_t steps, int64_t* steps_done) {
     if (!c || !y || !k1 || steps < 0) return HSGN_EINVAL;
-    CK(cudaSetDevice(c->device));
+    DeviceGuard dg_(c->device);
     hsgn_status st;
     const int CHUNK = 64;
     if ((st = ensure_ws(c, CHUNK))) return st;
@@ -1702,7 +1736,7 @@ extern "C" hsgn_status hsgn_bs3_fixed_steps(hsgn_ctx* c, hsgn_state* y, hsgn_sta
 extern "C" hsgn_status hsgn_profile_stages(hsgn_ctx* c, const hsgn_state* y, const hsgn_state* k1, double dt,
                                            int32_t reps, double* ms3) {
     if (!c || !y || !k1 || !ms3 || reps < 1) return HSGN_EINVAL;
-    CK(cudaSetDevice(c->device));
+    DeviceGuard dg_(c->device);
     hsgn_status st;
     if ((st = ensure_ws(c, 1))) return st;
     CK(cudaMemcpyAsync(c->ws[0].base - GHOST * c->grid.nx, y->base - GHOST * c->grid.nx, sizeof(double) * 5 * c->fs,
@@ -1763,7 +1797,7 @@ extern "C" hsgn_status hsgn_profile_fused(hsgn_ctx* c, const hsgn_state* y, cons
                                           int32_t reps, double* ms) {
     if (!c || !y || !k1 || !ms || reps < 1) return HSGN_EINVAL;
     if (c->nranks != 1) return fail(c, HSGN_EINVAL, "the fused kernel needs a whole-grid context");
-    CK(cudaSetDevice(c->device));
+    DeviceGuard dg_(c->device);
     hsgn_status st;
     if ((st = ensure_ws(c, 2))) return st;
     CK(cudaMemcpyAsync(c->ws[0].base - GHOST * c->grid.nx, y->base - GHOST * c->grid.nx, sizeof(double) * 5 * c->fs,
@@ -1911,6 +1945,7 @@ extern "C" {
 
 hsgn_status hsgn_group_create(const hsgn_grid* grid, const hsgn_phys* phys, const double* b_full, const int* devices,
                               int32_t n, hsgn_group** out) {
+    DeviceRestore dr_;
     if (!grid || !phys || !b_full || !out || n < 1 || grid->ny < 2 * n) return HSGN_EINVAL;
     hsgn_group* G = new hsgn_group();
     G->grid = *grid;
@@ -1970,6 +2005,7 @@ hsgn_status hsgn_group_create(const hsgn_grid* grid, const hsgn_phys* phys, cons
 }
 
 hsgn_status hsgn_group_destroy(hsgn_group* G) {
+    DeviceRestore dr_;
     if (!G) return HSGN_OK;
     for (int r = 0; r < (int)G->m.size(); ++r) {
         cudaSetDevice(G->m[r]->device);
@@ -1984,6 +2020,7 @@ hsgn_status hsgn_group_destroy(hsgn_group* G) {
 const char* hsgn_group_last_error(const hsgn_group* G) { return G ? G->err.c_str() : "null group"; }
 
 hsgn_status hsgn_group_state_alloc(hsgn_group* G, hsgn_gstate** out) {
+    DeviceRestore dr_;
     if (!G || !out) return HSGN_EINVAL;
     hsgn_gstate* s = new hsgn_gstate();
     for (hsgn_ctx* c : G->m) {
@@ -2000,6 +2037,7 @@ hsgn_status hsgn_group_state_alloc(hsgn_group* G, hsgn_gstate** out) {
 }
 
 hsgn_status hsgn_group_state_free(hsgn_group* G, hsgn_gstate* s) {
+    DeviceRestore dr_;
     if (!G || !s) return HSGN_EINVAL;
     for (size_t r = 0; r < s->p.size(); ++r) hsgn_state_free(G->m[r], s->p[r]);
     delete s;
@@ -2008,6 +2046,7 @@ hsgn_status hsgn_group_state_free(hsgn_group* G, hsgn_gstate* s) {
 
 // host layout: the full grid (5 fields of nx*ny); each member takes its rows
 hsgn_status hsgn_group_state_upload(hsgn_group* G, hsgn_gstate* s, const double* host) {
+    DeviceRestore dr_;
     if (!G || !s || !host) return HSGN_EINVAL;
     const long long nx = G->grid.nx, n = nx * G->grid.ny;
     for (int r = 0; r < G->n; ++r) {
@@ -2026,6 +2065,7 @@ hsgn_status hsgn_group_state_upload(hsgn_group* G, hsgn_gstate* s, const double*
 }
 
 hsgn_status hsgn_group_state_download(hsgn_group* G, const hsgn_gstate* s, double* host) {
+    DeviceRestore dr_;
     if (!G || !s || !host) return HSGN_EINVAL;
     const long long nx = G->grid.nx, n = nx * G->grid.ny;
     for (int r = 0; r < G->n; ++r) {
@@ -2043,6 +2083,7 @@ hsgn_status hsgn_group_state_download(hsgn_group* G, const hsgn_gstate* s, doubl
 
 // rhs on the decomposed grid (ghost rows of q must be current: upload does it)
 hsgn_status hsgn_group_rhs(hsgn_group* G, double t, const hsgn_gstate* q, hsgn_gstate* out, int64_t* bad_nodes) {
+    DeviceRestore dr_;
     if (!G || !q || !out) return HSGN_EINVAL;
     int64_t bad = 0;
     for (int r = 0; r < G->n; ++r) {
@@ -2072,6 +2113,7 @@ hsgn_status hsgn_group_rhs(hsgn_group* G, double t, const hsgn_gstate* q, hsgn_g
 // every stage (the NCCL schedule of enqueue_step with an in-process transport)
 hsgn_status hsgn_group_bs3_fixed_steps(hsgn_group* G, hsgn_gstate* y, hsgn_gstate* k1, double t, double dt,
                                        int64_t steps, int64_t* steps_done) {
+    DeviceRestore dr_;
     if (!G || !y || !k1 || steps < 0) return HSGN_EINVAL;
     const int n = G->n;
     for (hsgn_ctx* c : G->m) {
@@ -2160,6 +2202,7 @@ hsgn_status hsgn_group_bs3_fixed_steps(hsgn_group* G, hsgn_gstate* y, hsgn_gstat
 // global row order, one outer sum (kind: 0 mass, 1 energy, 2 energy rate).
 hsgn_status hsgn_group_reduce(hsgn_group* G, int32_t kind, const hsgn_gstate* q, const hsgn_gstate* qt,
                               double* out) {
+    DeviceRestore dr_;
     if (!G || !q || !out || kind < 0 || kind > 2 || (kind == 2 && !qt)) return HSGN_EINVAL;
     std::vector<double> rows(G->grid.ny);
     for (int r = 0; r < G->n; ++r) {
