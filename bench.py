@@ -180,7 +180,8 @@ def run_reference(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
             "config": {"workload": f"config 4 sample: {args.ref_n}^2 periodic MMS state, fixed-step BS3",
-                       "global_batch": 1, "seq_len": args.ref_n ** 2, "parallelism": "cpu-openmp"},
+                       "grid": f"{args.ref_n}x{args.ref_n}", "points": args.ref_n ** 2,
+                       "parallelism": "cpu-openmp"},
             "cpu_baseline": cb,
             "e2e": {"value": v, "unit": "point-stage updates/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
@@ -337,7 +338,7 @@ def main():
                 "data": "synthetic",
                 "config": {"workload": f"config 4: {n}x{nyg} periodic, manufactured bathymetry + state "
                                        f"(t=0.3), lambda=500, fixed-step BS3 dt=0.25dx/20",
-                           "global_batch": 1, "seq_len": n * nyg, "parallelism": f"slab{world}",
+                           "grid": f"{n}x{nyg}", "points": n * nyg, "parallelism": f"slab{world}",
                            "l2": "inputs > L2 (2.7 GB per state); no flush needed",
                            "rows_per_block": args.rows_per_block or "auto"},
                 "hbm_gbs": roofline["step_gbs"], "roofline": roofline, "cpu_baseline": cb, "e2e": e2e,
