@@ -164,6 +164,15 @@ def cpu_baseline(n_sample: int = 2048, steps: int = 12):
     return ref.describe(steps, ref.steps(steps))
 
 
+def workload_config(n: int, world: int) -> dict:
+    """The workload both arms report (BASELINE config 4; weak scaling stacks
+    8192-row slabs)."""
+    nyg = n * world
+    return {"workload": f"config 4: {n}x{nyg} periodic, manufactured bathymetry + state "
+                        f"(t=0.3), lambda=500, fixed-step BS3 dt=0.25dx/20",
+            "grid": f"{n}x{nyg}", "points": n * nyg, "parallelism": f"slab{world}"}
+
+
 def run_reference(args):
     """--impl reference: the reference's own CPU implementation, timed per
     step on this host's cores (rank 0 only under torchrun)."""
@@ -179,9 +188,10 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
-            "config": {"workload": f"config 4 sample: {args.ref_n}^2 periodic MMS state, fixed-step BS3",
-                       "grid": f"{args.ref_n}x{args.ref_n}", "points": args.ref_n ** 2,
-                       "parallelism": "cpu-openmp"},
+            # the same workload as the device arm; each step runs on the bounded
+            # sample cpu_baseline.sample states (host cores, OpenMP)
+            "config": dict(workload_config(args.n, args.gpus), parallelism="cpu-openmp",
+                           sample=f"{args.ref_n}x{args.ref_n} slice per step"),
             "cpu_baseline": cb,
             "e2e": {"value": v, "unit": "point-stage updates/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
@@ -336,11 +346,9 @@ def main():
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_all / args.steps,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic",
-                "config": {"workload": f"config 4: {n}x{nyg} periodic, manufactured bathymetry + state "
-                                       f"(t=0.3), lambda=500, fixed-step BS3 dt=0.25dx/20",
-                           "grid": f"{n}x{nyg}", "points": n * nyg, "parallelism": f"slab{world}",
-                           "l2": "inputs > L2 (2.7 GB per state); no flush needed",
-                           "rows_per_block": args.rows_per_block or "auto"},
+                "config": dict(workload_config(n, world),
+                               l2="inputs > L2 (2.7 GB per state); no flush needed",
+                               rows_per_block=args.rows_per_block or "auto"),
                 "hbm_gbs": roofline["step_gbs"], "roofline": roofline, "cpu_baseline": cb, "e2e": e2e,
                 "gpu_launches": kernels, "clocks": clk.summary(), "steps_done": done}
         print(json.dumps(line))
