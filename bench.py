@@ -214,6 +214,8 @@ def main():
     ap.add_argument("--fusion", type=int, default=-1, choices=[-1, 0, 1, 2, 3],
                     help="fixed-step kernel structure (0 per stage, 1 S31, 2 whole step, 3 S12 + S3; "
                          "-1 library default)")
+    ap.add_argument("--slab-ring", action="store_true",
+                    help="N=1 only: run the P-rank slab code path as a 1-rank NCCL ring (halos to itself)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -224,8 +226,13 @@ def main():
     import torch
     torch.cuda.set_device(local)
     dist = None
-    if world > 1:
+    if world > 1 or args.slab_ring:
         import torch.distributed as dist
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     import paper_2601_02540_b200 as H
@@ -234,10 +241,11 @@ def main():
 
     n = args.n
     nyg = n * world
-    g, q, b = mms_fields(n, nyg, 0.3) if world == 1 else S.slab_fields(n, nyg, 0.3, rank, world)
+    slabbed = world > 1 or args.slab_ring
+    g, q, b = mms_fields(n, nyg, 0.3) if not slabbed else S.slab_fields(n, nyg, 0.3, rank, world)
     dt = 0.25 * (2.0 / n) / 20.0
     phys = H.PhysSetup(9.81, 500.0, 1e-12, b.reshape(-1, n))
-    if world == 1:
+    if not slabbed:
         ctx = H.make_rhs_context(g, phys, device=local)
     else:
         ctx = S.make_slab_context(g, phys, rank, world, local, dist)
@@ -245,7 +253,7 @@ def main():
         ctx.set_rows_per_block(args.rows_per_block)
     if args.fusion >= 0:
         ctx.fused_stages = args.fusion
-    mode = ctx.fused_stages if world == 1 else 0
+    mode = ctx.fused_stages if not slabbed else (3 if ctx.fused_stages == 3 else 0)  # slabs: S12 + S3 or per stage
     y = ctx.state(q)
     k1 = ctx.state()
     H.rhs(ctx, 0.0, y, k1)
@@ -310,26 +318,35 @@ def main():
                                   "frac": value * BYTES_PER_POINT_STAGE / 1e9 / peak},
                 "step_gbs": step_bytes_per_node(mode, min(64, args.steps)) * points / (ms / args.steps * 1e-3) / 1e9}
 
-    # end-to-end through the public API with host buffers (pinned)
+    # end-to-end through the public API with host buffers (pinned); at N > 1
+    # every rank integrates its slab (halos and the step agreement over NCCL)
     e2e = None
-    if not args.no_e2e and world == 1:
+    if not args.no_e2e:
+        ny_l = ctx.ny_local
         host = torch.empty(q.size, dtype=torch.float64).pin_memory()
         host.numpy()[:] = q
         res_host = torch.empty(q.size, dtype=torch.float64).pin_memory()
-        st_in = H.StateField((n, n), host.numpy())
+        st_in = H.StateField((ny_l, n), host.numpy())
         cfg = H.IntegratorConfig(fixed_dt=dt)
         out_state = ctx.state()
         # warm
         H.adaptive_solve(ctx, st_in, 0.0, 2 * dt, cfg, out=out_state)
+        if dist:
+            dist.barrier()
         t0 = time.perf_counter()
         dq0 = ctx.state(st_in)                        # H2D of the host state
         rec = H.adaptive_solve(ctx, dq0, 0.0, args.steps * dt, cfg, out=out_state)
-        out_state.download(H.StateField((n, n), res_host.numpy()))  # D2H of the result
+        out_state.download(H.StateField((ny_l, n), res_host.numpy()))  # D2H of the result
         el = time.perf_counter() - t0
-        nbytes = 5 * points * 8
-        e2e = {"value": 3 * points * rec.accepted / el, "unit": "point-stage updates/s",
+        if dist:
+            t = torch.tensor([el], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = float(t.item())
+        nbytes = 5 * points * 8 * world
+        e2e = {"value": 3 * points * world * rec.accepted / el, "unit": "point-stage updates/s",
                "h2d_bytes_per_step": nbytes / args.steps, "d2h_bytes_per_step": nbytes / args.steps,
-               "api": "adaptive_solve(host q0 -> host q, fixed_dt, K steps) incl. initial RHS",
+               "api": "adaptive_solve(host q0 -> host q, fixed_dt, K steps) incl. initial RHS"
+                      + (" per slab rank, max over ranks" if world > 1 else ""),
                "wall_s": el}
         dq0.free()
         out_state.free()
@@ -348,7 +365,9 @@ def main():
                 "data": "synthetic",
                 "config": dict(workload_config(n, world),
                                l2="inputs > L2 (2.7 GB per state); no flush needed",
-                               rows_per_block=args.rows_per_block or "auto"),
+                               rows_per_block=args.rows_per_block or "auto",
+                               **({"parallelism": "slab1 as a 1-rank NCCL ring (the P-rank code path)"}
+                                  if slabbed and world == 1 else {})),
                 "hbm_gbs": roofline["step_gbs"], "roofline": roofline, "cpu_baseline": cb, "e2e": e2e,
                 "gpu_launches": kernels, "clocks": clk.summary(), "steps_done": done}
         print(json.dumps(line))

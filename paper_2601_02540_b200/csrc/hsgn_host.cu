@@ -47,7 +47,7 @@ cudaError_t launch_init_aux(const AuxArgs& A, double* q, cudaStream_t st);
 using namespace hsgn_dev;
 
 // ------------------------------------------------------------------ NCCL (dlopen)
-// The slab exchange needs five NCCL entry points; they are resolved at run
+// The slab exchange and the cross-rank agreement need a few NCCL entry points; they are resolved at run
 // time from the libnccl.so.2 already mapped by torch (or the system one), so
 // single-GPU use carries no NCCL dependency.
 namespace {
@@ -59,6 +59,7 @@ typedef int (*p_get_uid)(nccl_uid*);
 typedef int (*p_init_rank)(nccl_comm*, int, nccl_uid, int);
 typedef int (*p_send)(const void*, size_t, int, int, nccl_comm, cudaStream_t);
 typedef int (*p_recv)(void*, size_t, int, int, nccl_comm, cudaStream_t);
+typedef int (*p_allreduce)(const void*, void*, size_t, int, int, nccl_comm, cudaStream_t);
 typedef int (*p_group)(void);
 typedef int (*p_destroy)(nccl_comm);
 typedef const char* (*p_errstr)(int);
@@ -68,6 +69,7 @@ struct NcclApi {
     p_init_rank init_rank;
     p_send send;
     p_recv recv;
+    p_allreduce allreduce;
     p_group group_start, group_end;
     p_destroy destroy;
     p_errstr errstr;
@@ -84,15 +86,18 @@ const NcclApi& nccl() {
     api.init_rank = (p_init_rank)dlsym(h, "ncclCommInitRank");
     api.send = (p_send)dlsym(h, "ncclSend");
     api.recv = (p_recv)dlsym(h, "ncclRecv");
+    api.allreduce = (p_allreduce)dlsym(h, "ncclAllReduce");
     api.group_start = (p_group)dlsym(h, "ncclGroupStart");
     api.group_end = (p_group)dlsym(h, "ncclGroupEnd");
     api.destroy = (p_destroy)dlsym(h, "ncclCommDestroy");
     api.errstr = (p_errstr)dlsym(h, "ncclGetErrorString");
-    api.ok = api.get_uid && api.init_rank && api.send && api.recv && api.group_start && api.group_end &&
-             api.destroy;
+    api.ok = api.get_uid && api.init_rank && api.send && api.recv && api.allreduce && api.group_start &&
+             api.group_end && api.destroy;
     return api;
 }
+constexpr int NCCL_UINT64 = 5;   // ncclUint64
 constexpr int NCCL_FLOAT64 = 8;  // ncclDouble
+constexpr int NCCL_SUM = 0, NCCL_MIN = 3;
 }  // namespace
 
 // ------------------------------------------------------------------ types
@@ -130,6 +135,7 @@ struct hsgn_ctx {
     int forced_kind = -1;  // stencil kind override (tests); -1 = automatic
     int use_tma = 0;       // TMA staging of raw inputs when nx is even (opt-in: slower in r1)
     int in_group = 0;      // member of an in-process slab group (halo pulls by the group)
+    int ring1 = 0;         // 1-slab ring: NCCL attached to a 1-rank periodic-y context (halos to itself)
     int fused = 3;         // fixed-step graphs (whole-grid contexts): 0 per stage, 1 S31, 2 whole step, 3 S12 + S3
     int64_t n_evals = 0;
     std::string err;
@@ -236,10 +242,14 @@ double spacing(double lo, double hi, int n, int bounded) {  // grid.hpp:43-45
     return bounded ? (hi - lo) / (n - 1) : (hi - lo) / n;
 }
 
+// A single-domain context (wrap/clamp y edges, graph-captured fixed steps)
+// rather than a slab of a P-rank decomposition (ghost-row edges, halos).
+inline bool whole(const hsgn_ctx* c) { return c->nranks == 1 && !c->ring1; }
+
 // Global y edge modes of a slab.
 void slab_edges(const hsgn_ctx* c, int* lo, int* hi) {
     const bool yb = c->grid.kind_y == HSGN_BOUNDED;
-    if (c->nranks == 1) {
+    if (c->nranks == 1 && !c->ring1) {
         *lo = yb ? YE_CLAMP : YE_WRAP;
         *hi = yb ? YE_CLAMP : YE_WRAP;
         return;
@@ -343,28 +353,59 @@ static hsgn_status setup_ctx(hsgn_ctx* c) {
 // GHOST-1.  One grouped NCCL call per exchange, on the context stream
 // (graph-capturable).
 static hsgn_status exchange(hsgn_ctx* c, const hsgn_state* s, int nfields) {
-    if (c->nranks == 1 || c->in_group) return HSGN_OK;  // in a group the driver pulls halos
+    if ((c->nranks == 1 && !c->ring1) || c->in_group) return HSGN_OK;  // in a group the driver pulls halos
     if (!c->comm) return fail(c, HSGN_ENCCL, "slab context has no NCCL communicator attached");
     const NcclApi& N = nccl();
     const int nx = c->grid.nx;
     const bool yb = c->grid.kind_y == HSGN_BOUNDED;
     const int up = c->rank + 1 < c->nranks ? c->rank + 1 : (yb ? -1 : 0);
     const int dn = c->rank > 0 ? c->rank - 1 : (yb ? -1 : c->nranks - 1);
+    const size_t span = (size_t)GHOST * nx;  // GHOST contiguous rows per field and direction
+    // NCCL matches the k-th send to a peer with that peer's k-th receive from
+    // us.  With two ranks on a periodic ring (and a 1-rank ring) `up` and `dn`
+    // are the same peer, so every rank posts the upward leg (our top rows ->
+    // up's lower ghost rows) before the downward leg: the pairs then match
+    // for every P, including dn == up.
     int r = N.group_start();
     for (int f = 0; f < nfields && r == 0; ++f) {
         double* fld = s->f(f);
-        const size_t span = (size_t)GHOST * nx;  // GHOST contiguous rows per field and direction
-        if (dn >= 0) {
-            r |= N.send(fld, span, NCCL_FLOAT64, dn, c->comm, c->stream);
-            r |= N.recv(fld - span, span, NCCL_FLOAT64, dn, c->comm, c->stream);
-        }
-        if (up >= 0) {
-            r |= N.send(fld + (long long)(c->ny_loc - GHOST) * nx, span, NCCL_FLOAT64, up, c->comm, c->stream);
-            r |= N.recv(fld + (long long)c->ny_loc * nx, span, NCCL_FLOAT64, up, c->comm, c->stream);
-        }
+        if (up >= 0) r |= N.send(fld + (long long)(c->ny_loc - GHOST) * nx, span, NCCL_FLOAT64, up, c->comm, c->stream);
+        if (dn >= 0) r |= N.recv(fld - span, span, NCCL_FLOAT64, dn, c->comm, c->stream);
+        if (dn >= 0) r |= N.send(fld, span, NCCL_FLOAT64, dn, c->comm, c->stream);
+        if (up >= 0) r |= N.recv(fld + (long long)c->ny_loc * nx, span, NCCL_FLOAT64, up, c->comm, c->stream);
     }
     r |= N.group_end();
     if (r) return fail(c, HSGN_ENCCL, "ncclSend/Recv halo exchange failed (%d)", r);
+    return HSGN_OK;
+}
+
+// Cross-rank agreement of a P-rank decomposition.  Every decision the
+// reference takes on a global quantity (depth failures, min depth, the
+// adaptive error norm, the start-step norms) must be identical on all ranks,
+// or their step sequences -- and the halo exchanges pairing them -- diverge.
+// The rank-local device values are summed / min-reduced in place on the
+// context stream before the host reads them (graph-capturable, no host sync).
+static bool multi_rank(const hsgn_ctx* c) { return c->nranks > 1 && !c->in_group; }
+
+static hsgn_status agree(hsgn_ctx* c, void* d, size_t count, int dtype, int op) {
+    if (!multi_rank(c)) return HSGN_OK;
+    if (!c->comm) return fail(c, HSGN_ENCCL, "slab context has no NCCL communicator attached");
+    const int r = nccl().allreduce(d, d, count, dtype, op, c->comm, c->stream);
+    if (r) return fail(c, HSGN_ENCCL, "ncclAllReduce failed (%d)", r);
+    return HSGN_OK;
+}
+
+// A step record: depth-failure counts summed, min(ynew.h) bit pattern
+// min-reduced (positive doubles order as their bit patterns), one NCCL group.
+static hsgn_status agree_rec(hsgn_ctx* c, StepRec* rec) {
+    if (!multi_rank(c) || !rec) return HSGN_OK;
+    const NcclApi& N = nccl();
+    int r = N.group_start();
+    hsgn_status s = agree(c, rec->bad, 3, NCCL_UINT64, NCCL_SUM);
+    if (!s) s = agree(c, &rec->minh, 1, NCCL_UINT64, NCCL_MIN);
+    r |= N.group_end();
+    if (s) return s;
+    if (r) return fail(c, HSGN_ENCCL, "ncclGroupEnd failed (%d)", r);
     return HSGN_OK;
 }
 
@@ -606,6 +647,7 @@ static hsgn_status enqueue_chunk_s12(hsgn_ctx* c, int parity, int steps, double 
                              R->d_gauge + (size_t)s * R->gi.size(), c->stream));
         if ((st = enqueue_s3_fixed(c, Y[p ^ 1], K[p ^ 1], rec, dt))) return st;
         if ((st = exchange(c, K[p ^ 1], 5))) return st;
+        if ((st = agree_rec(c, rec))) return st;  // the next S12 halts on the global record
     }
     return HSGN_OK;
 }
@@ -652,11 +694,13 @@ static hsgn_status enqueue_step(hsgn_ctx* c, const hsgn_state* y, const hsgn_sta
                                 const StepRec* prev, double t, double dt, bool adaptive, double atol,
                                 double rtol, int64_t* kernels) {
     hsgn_state* produced[3] = {k2, ynew, k4};
+    hsgn_status s0;
     for (int stage = 1; stage <= 3; ++stage) {
         hsgn_status s = enqueue_stage(c, stage, y, k1, k2, ynew, k4, part, rec, prev, t, dt, adaptive, atol, rtol);
         if (s) return s;
         if ((s = exchange(c, produced[stage - 1], 5))) return s;
     }
+    if ((s0 = agree_rec(c, rec))) return s0;
     if (kernels) *kernels += 3;
     return HSGN_OK;
 }
@@ -688,6 +732,7 @@ static hsgn_status rhs_checked(hsgn_ctx* c, double t, const hsgn_state* q, hsgn_
     unsigned long long* d_bad = &c->d_rec[0].bad[0];
     CK(cudaMemsetAsync(d_bad, 0, sizeof(unsigned long long), c->stream));
     CK(launch_depth_check(q->base, (long long)c->ny_loc * c->grid.nx, d_bad, c->stream));
+    if ((s = agree(c, d_bad, 1, NCCL_UINT64, NCCL_SUM))) return s;
     unsigned long long hb = 0;
     CK(cudaMemcpyAsync(&hb, d_bad, sizeof hb, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
@@ -833,6 +878,15 @@ hsgn_status hsgn_ctx_attach_nccl(hsgn_ctx* c, const unsigned char nccl_id[128]) 
     DeviceGuard dg_(c->device);
     int r = N.init_rank(&c->comm, c->nranks, id, c->rank);
     if (r) return fail(c, HSGN_ENCCL, "ncclCommInitRank failed (%d)", r);
+    if (c->nranks == 1 && c->grid.kind_y != HSGN_BOUNDED && !c->ring1) {
+        // a 1-rank periodic communicator: the context becomes a 1-slab ring
+        // (ghost-row edges, halos sent to itself), i.e. exactly the P-rank
+        // code path at P = 1 (the slab schedule without a second GPU)
+        if (c->ws_ready || !c->graphs.empty())
+            return fail(c, HSGN_EINVAL, "attach the communicator before the first integration");
+        c->ring1 = 1;
+        setup_ctx(c);  // re-derives the edge modes, stencil kind and launch shape
+    }
     // exchange b's ghost rows once (static field)
     hsgn_state bs;
     bs.base = c->b;
@@ -1095,10 +1149,10 @@ hsgn_status get_fixed_graph(hsgn_ctx* c, int steps, int parity, double dt, const
     CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
     reset_recs(c, steps);
     hsgn_status st = HSGN_OK;
-    if (c->fused == 1 && c->nranks == 1) st = enqueue_chunk_fused(c, parity, steps, dt, R, nullptr);
-    if (c->fused == 2 && c->nranks == 1) st = enqueue_chunk_step(c, parity, steps, dt, R);
-    if (c->fused == 3 && c->nranks == 1) st = enqueue_chunk_s12(c, parity, steps, dt, R);
-    for (int s = 0; s < steps && !st && !(c->fused && c->nranks == 1); ++s) {
+    if (c->fused == 1 && whole(c)) st = enqueue_chunk_fused(c, parity, steps, dt, R, nullptr);
+    if (c->fused == 2 && whole(c)) st = enqueue_chunk_step(c, parity, steps, dt, R);
+    if (c->fused == 3 && whole(c)) st = enqueue_chunk_s12(c, parity, steps, dt, R);
+    for (int s = 0; s < steps && !st && !(c->fused && whole(c)); ++s) {
         const int p = (parity + s) & 1;
         st = enqueue_step(c, Y[p], K[p], &c->ws[4], Y[p ^ 1], K[p ^ 1], nullptr, &c->d_rec[s],
                           s ? &c->d_rec[s - 1] : nullptr, 0.0, dt, false, 0, 0, nullptr);
@@ -1136,7 +1190,7 @@ static hsgn_status run_fixed_chunk(hsgn_ctx* c, int parity, int steps, double t,
     const bool gauges = R && !R->gi.empty();
     hsgn_status st;
     if ((st = ensure_ws(c, steps))) return st;
-    if (c->source == 0 && c->nranks == 1) {
+    if (c->source == 0 && whole(c)) {
         FixedGraph* fg = nullptr;
         if ((st = get_fixed_graph(c, steps, parity, dt, R, &fg))) return st;
         CK(cudaGraphLaunch(fg->exec, c->stream));
@@ -1203,10 +1257,12 @@ static hsgn_status wrms(hsgn_ctx* c, const hsgn_state* x, const hsgn_state* ref,
     const long long n = (long long)c->ny_loc * c->grid.nx;
     CK(launch_wrms(x->base, ref->base, atol, rtol, n, c->fs, c->d_err_part, c->stream));
     CK(launch_sum_partials(c->d_err_part, wrms_blocks(), c->d_scalar, c->stream));
+    hsgn_status st = agree(c, c->d_scalar, 1, NCCL_FLOAT64, NCCL_SUM);
+    if (st) return st;
     double s = 0;
     CK(cudaMemcpyAsync(&s, c->d_scalar, sizeof s, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
-    *out = std::sqrt(s / (double)(5 * n));
+    *out = std::sqrt(s / (5.0 * (double)c->grid.nx * (double)c->grid.ny));  // global node count
     return HSGN_OK;
 }
 
@@ -1216,6 +1272,7 @@ static hsgn_status rhs_eval(hsgn_ctx* c, double t, const hsgn_state* q, hsgn_sta
     CK(cudaMemsetAsync(d_bad, 0, sizeof(unsigned long long), c->stream));
     hsgn_status s = rhs_raw(c, t, q, out, false, d_bad);
     if (s) return s;
+    if ((s = agree(c, d_bad, 1, NCCL_UINT64, NCCL_SUM))) return s;
     unsigned long long hb = 0;
     CK(cudaMemcpyAsync(&hb, d_bad, sizeof hb, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
@@ -1483,13 +1540,17 @@ extern "C" hsgn_status hsgn_solve_recorded(hsgn_ctx* c, const hsgn_state* q0, do
                 st = enqueue_stage(c, 3, &c->ws[p], &c->ws[2 + p], &c->ws[4], &c->ws[q], &c->ws[2 + q], &c->ws[5],
                                    &c->d_rec[0], nullptr, t, dt, !fixed, cfg->abs_tol, cfg->rel_tol);
             if (!st) st = exchange(c, &c->ws[2 + q], 5);
+            if (!st) st = agree_rec(c, &c->d_rec[0]);
             kernels += 2;
         } else {
             st = enqueue_step(c, &c->ws[p], &c->ws[2 + p], &c->ws[4], &c->ws[q], &c->ws[2 + q], &c->ws[5],
                               &c->d_rec[0], nullptr, t, dt, !fixed, cfg->abs_tol, cfg->rel_tol, &kernels);
         }
         if (st) return st;
-        if (!fixed) CK(launch_sum_partials(c->d_err_part, stage_grid_blocks(c->base), c->d_scalar, c->stream));
+        if (!fixed) {
+            CK(launch_sum_partials(c->d_err_part, stage_grid_blocks(c->base), c->d_scalar, c->stream));
+            if ((st = agree(c, c->d_scalar, 1, NCCL_FLOAT64, NCCL_SUM))) return st;
+        }
         StepRec r;
         double err_sum = 0.0;
         CK(cudaMemcpyAsync(&r, &c->d_rec[0], sizeof r, cudaMemcpyDeviceToHost, c->stream));
@@ -1513,7 +1574,7 @@ extern "C" hsgn_status hsgn_solve_recorded(hsgn_ctx* c, const hsgn_state* q0, do
         double err = 0.0, min_h = std::numeric_limits<double>::infinity();
         if (r.minh != ~0ull) std::memcpy(&min_h, &r.minh, 8);
         if (!fixed) {
-            const double n5 = 5.0 * (double)((long long)c->ny_loc * c->grid.nx);
+            const double n5 = 5.0 * (double)c->grid.nx * (double)c->grid.ny;  // global node count
             err = std::sqrt(err_sum / n5);
         }
         const bool accept = fixed || err <= 1.0;
@@ -1562,7 +1623,7 @@ extern "C" hsgn_status hsgn_recorder_create(hsgn_ctx* c, int32_t n_gauges, const
     *out = nullptr;
     if (conservation_stride < 1)  // config.hpp:234-237
         return fail(c, HSGN_EINVAL, "conservation_stride must be >= 1");
-    if (c->nranks != 1) return fail(c, HSGN_EINVAL, "the recorder needs a whole-grid context");
+    if (!whole(c)) return fail(c, HSGN_EINVAL, "the recorder needs a whole-grid context");
     DeviceGuard dg_(c->device);
     hsgn_recorder* R = new hsgn_recorder;
     R->c = c;
@@ -1796,7 +1857,8 @@ extern "C" hsgn_status hsgn_profile_stages(hsgn_ctx* c, const hsgn_state* y, con
 extern "C" hsgn_status hsgn_profile_fused(hsgn_ctx* c, const hsgn_state* y, const hsgn_state* k1, double dt,
                                           int32_t reps, double* ms) {
     if (!c || !y || !k1 || !ms || reps < 1) return HSGN_EINVAL;
-    if (c->nranks != 1) return fail(c, HSGN_EINVAL, "the fused kernel needs a whole-grid context");
+    if (!whole(c) && c->fused != 3)  // slabs run S12 + S3 (or the per-stage kernels)
+        return fail(c, HSGN_EINVAL, "the S31 / whole-step kernels need a whole-grid context");
     DeviceGuard dg_(c->device);
     hsgn_status st;
     if ((st = ensure_ws(c, 2))) return st;
