@@ -262,6 +262,34 @@ hsgn_status hsgn_group_bs3_fixed_steps(hsgn_group* g, hsgn_gstate* y, hsgn_gstat
 hsgn_status hsgn_group_reduce(hsgn_group* g, int32_t kind, const hsgn_gstate* q, const hsgn_gstate* q_t,
                               double* out);
 
+/* ------------------------------------------------------------ scenarios (CLI front end) */
+
+/* The reference scenario registry (scenarios.hpp:18-707): make_scenario
+ * resolves a scenario by name with numeric parameter overrides (same names,
+ * defaults and messages, :598-698); sample() evaluates its initial b, h, u, v
+ * at the nodes of an nx x ny grid over `domain` (w and eta are left zero for
+ * hsgn_init_auxiliary, as prepare_run does, :55-78); exact() fills the exact
+ * state at time t (soliton, manufactured).  Host-side, no device needed. */
+typedef struct {
+    char name[32];
+    hsgn_grid domain; /* extents and kinds; nx, ny = the scenario's default resolution */
+    double g, lambda, t0, t_final;
+    int32_t has_source; /* manufactured forcing: hsgn_set_source(ctx, 1) */
+    int32_t has_exact;
+    int32_t n_exact_vars, exact_vars[5]; /* field indices compared by the convergence study */
+    int32_t n_gauges, n_snapshots;
+    double gauges[8][2];
+    double snapshot_times[8];
+    int32_t kind, reserved;
+    double p[24]; /* resolved parameters and derived constants (private) */
+} hsgn_scenario;
+int32_t hsgn_scenario_count(void);
+const char* hsgn_scenario_name(int32_t k); /* scenario_names(), scenarios.hpp:700-705 */
+hsgn_status hsgn_scenario_make(const char* name, const char* const* keys, const double* vals, int32_t n,
+                               hsgn_scenario* out, char* err, int32_t err_len);
+hsgn_status hsgn_scenario_sample(const hsgn_scenario* s, int32_t nx, int32_t ny, double* b, double* q5);
+hsgn_status hsgn_scenario_exact(const hsgn_scenario* s, int32_t nx, int32_t ny, double t, double* q5);
+
 /* ------------------------------------------------------------ misc */
 hsgn_status hsgn_synchronize(hsgn_ctx* ctx);
 /* Elapsed ms of the last hsgn_bs3_fixed_steps call measured with CUDA events

@@ -11,6 +11,7 @@
 // prebuilt file.  Never linked by the product library.
 
 #include <hsgn/analysis.hpp>
+#include <hsgn/config.hpp>
 #include <hsgn/io.hpp>
 #include <hsgn/manufactured_generated.hpp>
 #include <hsgn/model.hpp>
@@ -21,8 +22,10 @@
 #include <hsgn/time_integration.hpp>
 
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <map>
+#include <sstream>
 #include <string>
 
 #include "oracle_abi.h"
@@ -400,6 +403,60 @@ void ref_mms_exact_field(const orc_grid* g, double t, double* q) {
             for (int k = 0; k < 5; ++k)
                 q[k * n + static_cast<std::size_t>(j) * grid.nx + i] = s[k];
         }
+}
+
+// parse_config_text (config.hpp:139-247) with a canonical dump of every
+// RunConfig field (%.17g numbers, one "key=value" per line) for the
+// differential tests of paper_2601_02540_b200/config.py.  Returns 0, or -1
+// with the exception message in out.
+int ref_parse_config(const char* text, char* out, int out_len) {
+    std::ostringstream o;
+    auto num = [&](const char* k, double v) {
+        char b[64];
+        std::snprintf(b, sizeof b, "%.17g", v);
+        o << k << '=' << b << '\n';
+    };
+    try {
+        RunConfig c = parse_config_text(text);
+        o << "scenario=" << c.scenario << '\n';
+        for (const auto& [k, v] : c.scenario_params) num(("param." + k).c_str(), v);
+        num("nx", c.nx);
+        num("ny", c.ny);
+        num("t0", c.t0);
+        num("t_final", c.t_final);
+        num("threads", c.threads);
+        num("abs_tol", c.integrator.abs_tol);
+        num("rel_tol", c.integrator.rel_tol);
+        num("dt_initial", c.integrator.dt_initial);
+        num("dt_max", c.integrator.dt_max);
+        num("fixed_dt", c.integrator.fixed_dt);
+        num("max_steps", (double)c.integrator.max_steps);
+        num("safety", c.integrator.safety);
+        num("growth_cap", c.integrator.growth_cap);
+        num("shrink_floor", c.integrator.shrink_floor);
+        num("tolerances_set", c.tolerances_set);
+        o << "output_dir=" << c.output_dir << '\n';
+        num("gauges_set", c.gauges_set);
+        for (const auto& g : c.gauges) {
+            num("gauge.x", g[0]);
+            num("gauge.y", g[1]);
+        }
+        num("snapshots_set", c.snapshots_set);
+        for (double t : c.snapshot_times) num("snapshot", t);
+        num("conservation_stride", (double)c.conservation_stride);
+        num("cross_section_set", c.cross_section_set);
+        num("cross_section_y", c.cross_section_y);
+        for (int r : c.resolutions) num("resolution", r);
+        num("converge_ny", c.converge_ny);
+        for (int r : c.bench_resolutions) num("bench_resolution", r);
+        num("bench_repetitions", c.bench_repetitions);
+        num("bench_warmups", c.bench_warmups);
+    } catch (const std::exception& e) {
+        std::snprintf(out, (size_t)out_len, "%s", e.what());
+        return -1;
+    }
+    std::snprintf(out, (size_t)out_len, "%s", o.str().c_str());
+    return 0;
 }
 
 }  // extern "C"

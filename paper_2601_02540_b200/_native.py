@@ -43,6 +43,13 @@ class hsgn_record(C.Structure):
                 ("rhs_evals_setup", I64), ("aborted", I32), ("reason", C.c_char * 256)]
 
 
+class hsgn_scenario(C.Structure):
+    _fields_ = [("name", C.c_char * 32), ("domain", hsgn_grid), ("g", D), ("lambda_", D), ("t0", D),
+                ("t_final", D), ("has_source", I32), ("has_exact", I32), ("n_exact_vars", I32),
+                ("exact_vars", I32 * 5), ("n_gauges", I32), ("n_snapshots", I32), ("gauges", (D * 2) * 8),
+                ("snapshot_times", D * 8), ("kind", I32), ("reserved", I32), ("p", D * 24)]
+
+
 CTX = C.c_void_p
 STATE = C.c_void_p
 OBSERVER = C.CFUNCTYPE(None, D, STATE, STATE, C.c_void_p)
@@ -125,6 +132,12 @@ def lib() -> C.CDLL:
     f("hsgn_recorder_gauges", C.c_int, REC, PD, PD)
     f("hsgn_recorder_conservation", C.c_int, REC, PD)
     f("hsgn_recorder_snapshot", C.c_int, REC, I32, PD, PD, PD)
+    SC = C.POINTER(hsgn_scenario)
+    f("hsgn_scenario_count", I32)
+    f("hsgn_scenario_name", C.c_char_p, I32)
+    f("hsgn_scenario_make", C.c_int, C.c_char_p, C.POINTER(C.c_char_p), PD, I32, SC, C.c_char_p, I32)
+    f("hsgn_scenario_sample", C.c_int, SC, I32, I32, PD, PD)
+    f("hsgn_scenario_exact", C.c_int, SC, I32, I32, D, PD)
     _lib = L
     return L
 
@@ -145,4 +158,6 @@ EXPORTS = [
     "hsgn_recorder_create", "hsgn_recorder_destroy", "hsgn_solve_recorded", "hsgn_recorder_counts",
     "hsgn_recorder_gauge_node", "hsgn_recorder_gauges", "hsgn_recorder_conservation", "hsgn_recorder_snapshot",
     "hsgn_set_fused_stages", "hsgn_fused_stages", "hsgn_profile_fused",
+    "hsgn_scenario_count", "hsgn_scenario_name", "hsgn_scenario_make", "hsgn_scenario_sample",
+    "hsgn_scenario_exact",
 ]

@@ -17,7 +17,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.environ.get("HSGN_BUILD_DIR") or os.path.join(HERE, "_native")  # variants: experiments only
 LIB = os.path.join(OUT_DIR, "libhsgn_b200.so")
-SOURCES = ["sgn_stage.cu", "sgn_aux.cu", "hsgn_host.cu"]
+SOURCES = ["sgn_stage.cu", "sgn_aux.cu", "hsgn_host.cu", "hsgn_scenarios.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
 
@@ -45,9 +45,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objs = []
     log = []
     for src in SOURCES:
-        obj = os.path.join(OUT_DIR, src.replace(".cu", ".o"))
+        obj = os.path.join(OUT_DIR, os.path.splitext(src)[0] + ".o")
         extra = os.environ.get("HSGN_NVCC_EXTRA", "").split()  # experiments only (e.g. -DHSGN_MIN_BLOCKS=4)
-        cmd = [nvcc(), *ARCH, *FLAGS, *extra, "-c", os.path.join(CSRC, src), "-o", obj]
+        # host C++ (the scenario registry): no FP contraction, like the reference build
+        host = ["-Xcompiler", "-ffp-contract=off"] if src.endswith(".cpp") else []
+        cmd = [nvcc(), *ARCH, *FLAGS, *host, *extra, "-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         log.append(r.stdout + r.stderr)
         if r.returncode != 0:

@@ -89,6 +89,7 @@ def test_struct_layouts_match_header():
     assert ctypes.sizeof(N.hsgn_phys) == 3 * 8
     assert ctypes.sizeof(N.hsgn_cfg) == 10 * 8
     assert ctypes.sizeof(N.hsgn_record) == 8 + 4 * 8 + 4 + 256 + 4  # trailing pad to 8
+    assert ctypes.sizeof(N.hsgn_scenario) == 32 + 48 + 4 * 8 + 8 * 4 + 2 * 4 + 16 * 8 + 8 * 8 + 2 * 4 + 24 * 8
 
 
 def test_host_api_validation_without_gpu():
