@@ -47,12 +47,17 @@ constexpr int WX = BX - 2;  // finished columns per tile
 
 template <int MODE>
 __host__ __device__ constexpr int npairs() { return MODE == MODE_S2 ? NPAIRS_S2 : NPAIRS; }
+#ifndef HSGN_S3_WARPS
+#define HSGN_S3_WARPS 20  // resident warps per SM asked of the fixed-step stage-3 kernel
+#endif
 template <int MODE>
 __host__ __device__ constexpr int min_blocks() {
     // measured (r1): S2 (largest ring, 16 raw inputs) is best at 3 CTAs/SM;
     // the other stages fit 96 registers without spills and run best at 5
     // (expressed as resident warps per SM: 12 for S2, 20 for the others)
-    return HSGN_MIN_BLOCKS > 0 ? HSGN_MIN_BLOCKS : (MODE == MODE_S2 ? 12 : MODE == MODE_S3A ? 16 : 20) / (BX / 32);
+    return HSGN_MIN_BLOCKS > 0 ? HSGN_MIN_BLOCKS
+                               : (MODE == MODE_S2 ? 12 : MODE == MODE_S3A ? 16 : MODE == MODE_S3 ? HSGN_S3_WARPS : 20) /
+                                     (BX / 32);
 }
 
 // Per-field device pointers (kernel parameters live in the constant bank, so

@@ -204,3 +204,124 @@ def test_cli_run_abort_exit_code(tmp_path):
     rc = cli.main(["run", "--config", _write_cfg(tmp_path, text), "--output", ddir])
     meta = json.loads(_read(os.path.join(ddir, "run_meta.json")))
     assert rc == 1 and meta["status"] == "aborted" and "depth" in meta["abort_reason"]
+
+
+# ------------------------------------------------------------------ the reference's test_cli.cpp cases
+
+def _cfg(**kw):
+    from paper_2601_02540_b200.config import RunConfig
+    c = RunConfig()
+    for k, v in kw.items():
+        setattr(c, k, v)
+    return c
+
+
+def test_ref_cli_run_full_output_set(tmp_path):
+    """test_cli.cpp:62-132"""
+    d = str(tmp_path / "run_lake")
+    cfg = _cfg(scenario="lake_at_rest", nx=20, ny=20, t_final=1.0, output_dir=d, gauges_set=True,
+               gauges=[(0.0, 0.0)], snapshots_set=True, snapshot_times=[0.0, 0.5], cross_section_set=True,
+               cross_section_y=0.0)
+    assert cli.cmd_run(cfg, open(os.devnull, "w")) == 0
+    for f in ("conservation.csv", "gauges.csv", "run_meta.json", "cross_section.csv", "snapshot_t0.csv",
+              "snapshot_t0.5.csv"):
+        assert os.path.exists(os.path.join(d, f)), f
+    assert _read(os.path.join(d, "conservation.csv")).splitlines()[0] == \
+        "t,total_mass,total_energy,semidiscrete_energy_rate"
+    cons = _table(os.path.join(d, "conservation.csv"))
+    assert len(cons) >= 2
+    m0, e0 = cons[0, 1], cons[0, 2]
+    assert np.all(np.abs(cons[:, 1] - m0) <= 1e-12 * abs(m0))
+    assert np.all(np.abs(cons[:, 2] - e0) <= 1e-12 * abs(e0))
+    assert np.all(np.abs(cons[:, 3]) <= 1e-11 * abs(e0))
+    g = _table(os.path.join(d, "gauges.csv"))
+    assert [ln for ln in _read(os.path.join(d, "gauges.csv")).splitlines() if not ln.startswith("#")][0] == \
+        "t,gauge_1"
+    assert np.all(np.abs(g[:, 1] - 1.0) <= 1e-12)
+    meta = json.loads(_read(os.path.join(d, "run_meta.json")))
+    assert meta["status"] == "ok" and meta["command"] == "run" and meta["scenario"]["name"] == "lake_at_rest"
+    assert meta["grid"]["nx"] == 20 and meta["grid"]["boundary_x"] == "periodic"
+    assert meta["time"]["t_reached"] == 1.0
+    st = meta["steps"]
+    assert st["rhs_evals"] == 3 * (st["accepted"] + st["rejected"]) + 1 + st["rhs_evals_setup"]
+    assert abs(meta["conservation"]["mass_drift_rel"]) <= 1e-12
+    assert len(meta["snapshots"]) == 2 and meta["snapshots"][0]["target"] == 0.0
+    assert meta["snapshots"][0]["file"] == "snapshot_t0.csv"
+    snap = _read(os.path.join(d, "snapshot_t0.5.csv")).splitlines()
+    assert snap[0] == "x,y,h,u,v,w,eta,b" and len(snap) == 1 + 20 * 20
+
+
+def test_ref_cli_reruns_byte_identical(tmp_path):
+    """test_cli.cpp:134-156 (adaptive run: the device sums are deterministic)."""
+    dirs = []
+    for name in ("rerun_a", "rerun_b"):
+        d = str(tmp_path / name)
+        cfg = _cfg(scenario="lake_at_rest", nx=16, ny=16, t_final=0.5, output_dir=d, gauges_set=True,
+                   gauges=[(1.0, -1.0)], snapshots_set=True, snapshot_times=[0.25])
+        assert cli.cmd_run(cfg, open(os.devnull, "w")) == 0
+        dirs.append(d)
+    for f in ("conservation.csv", "gauges.csv", "snapshot_t0.25.csv"):
+        assert _read(os.path.join(dirs[0], f)) == _read(os.path.join(dirs[1], f))
+
+
+def test_ref_cli_abort_partial_record(tmp_path):
+    """test_cli.cpp:158-178"""
+    d = str(tmp_path / "run_abort")
+    cfg = _cfg(scenario="lake_at_rest", nx=16, ny=16, t_final=5.0, output_dir=d)
+    cfg.integrator.max_steps = 1
+    assert cli.cmd_run(cfg, open(os.devnull, "w")) == 1
+    meta = json.loads(_read(os.path.join(d, "run_meta.json")))
+    assert meta["status"] == "aborted" and "step budget" in meta["abort_reason"]
+    assert meta["time"]["t_reached"] < 5.0
+    assert len(_table(os.path.join(d, "conservation.csv"))) >= 1
+
+
+def test_ref_cli_unknown_scenario_touches_no_disk(tmp_path):
+    """test_cli.cpp:180-187"""
+    d = str(tmp_path / "should_not_exist")
+    with pytest.raises(ValueError):
+        cli.cmd_run(_cfg(scenario="maelstrom", output_dir=d), open(os.devnull, "w"))
+    assert not os.path.exists(d)
+
+
+def test_ref_cli_converge_ladder(tmp_path):
+    """test_cli.cpp:189-228"""
+    d = str(tmp_path / "converge_mms")
+    cfg = _cfg(scenario="manufactured", t_final=0.5, resolutions=[16, 32], tolerances_set=True, output_dir=d)
+    cfg.integrator.abs_tol = 1e-8
+    cfg.integrator.rel_tol = 1e-8
+    assert cli.cmd_converge(cfg, open(os.devnull, "w")) == 0
+    rows = _read(os.path.join(d, "convergence.csv")).splitlines()
+    head = rows[0].split(",")
+    assert len(head) == 2 + 2 * 5 + 1 and head[:3] == ["nx", "dx", "err_h"] and head[-1] == "status"
+    t = [r.split(",") for r in rows[1:]]
+    assert len(t) == 2 and float(t[0][0]) == 16.0 and float(t[1][0]) == 32.0
+    assert float(t[1][2]) < float(t[0][2])
+    meta = json.loads(_read(os.path.join(d, "run_meta.json")))
+    assert meta["status"] == "ok" and meta["row_status"][0] == "ok"
+    bad = _cfg(**{**vars(cfg), "scenario": "still_water"})
+    with pytest.raises(ValueError, match="no exact solution"):
+        cli.cmd_converge(bad, open(os.devnull, "w"))
+    bad = _cfg(**{**vars(cfg), "resolutions": [8]})
+    with pytest.raises(ValueError, match=">= 2"):
+        cli.cmd_converge(bad, open(os.devnull, "w"))
+
+
+def test_ref_cli_bench_ladder(tmp_path):
+    """test_cli.cpp:230-266"""
+    d = str(tmp_path / "bench_small")
+    cfg = _cfg(bench_resolutions=[4, 6, 8], bench_repetitions=3, bench_warmups=1, output_dir=d)
+    assert cli.cmd_bench(cfg, open(os.devnull, "w")) == 0
+    rows = _read(os.path.join(d, "bench.csv")).splitlines()
+    assert rows[0].split(",") == ["nx", "ny", "n_total", "seconds_per_rhs", "seconds_per_rhs_min", "threads"]
+    assert len(rows) == 4
+    for r in rows[1:]:
+        v = [float(x) for x in r.split(",")]
+        assert v[2] == v[0] * v[1] and v[3] > 0 and v[4] > 0 and v[4] <= v[3]
+    bad_dir = str(tmp_path / "bench_bad")
+    with pytest.raises(ValueError, match="4-node minimum"):
+        cli.cmd_bench(_cfg(**{**vars(cfg), "bench_resolutions": [2, 4], "output_dir": bad_dir}),
+                      open(os.devnull, "w"))
+    assert not os.path.exists(bad_dir)
+    with pytest.raises(ValueError, match="repetitions"):
+        cli.cmd_bench(_cfg(**{**vars(cfg), "bench_repetitions": 0}), open(os.devnull, "w"))
