@@ -1,6 +1,13 @@
 """GPU: the reference acceptance gates that exercise the physics of the path
-(acceptance_main.cpp c7-c9), run on the device with initial states from the
-reference's own scenario library (oracle/_ref: make_scenario + prepare_run).
+(acceptance_main.cpp c5-c9), run on the device with initial states from the
+reference's own scenario library (oracle/_ref: make_scenario + prepare_run)
+or, for the convergence gates, from the product's own registry and
+refinement driver (scenarios.py, cli.run_convergence_study).
+
+c5  solitary wave {200, 400, 800} x 4, lambda = 30000, tol 1e-10: orders of
+    h, u at the finest pair in (1.8, 2.2)
+c6  manufactured solution {32, 64, 128}^2, periodic and reflecting, tol
+    1e-10: orders of all five fields at the finest pair in (1.8, 2.2)
 
 c7  dam break: plateau depth within 0.02 and leading crest within 0.04 of
     riemann_predictions(1.8, 1.0, g) (scenarios.hpp:410-428)
@@ -88,3 +95,25 @@ def test_c9_energy_drift_shrinks_with_tolerance(ref):
         assert not sol.aborted, sol.abort_reason
         drift.append(abs(H.total_energy(ctx, sol.q) - e0) / e0)
     assert drift[1] < drift[0], drift
+
+
+def test_c5_soliton_order():
+    """acceptance_main.cpp:162-178 on the device."""
+    from paper_2601_02540_b200 import cli
+    from paper_2601_02540_b200.scenarios import make_scenario
+    spec = make_scenario("soliton")
+    t = cli.run_convergence_study(spec, [200, 400, 800], H.IntegratorConfig(abs_tol=1e-10, rel_tol=1e-10),
+                                  ny_fixed=4)
+    assert t.status == ["ok"] * 3 and t.variables == ["h", "u"]
+    assert all(1.8 < r < 2.2 for r in t.rates[-1]), t.rates
+
+
+@pytest.mark.parametrize("bounded", [0.0, 1.0])
+def test_c6_manufactured_order(bounded):
+    """acceptance_main.cpp:180-203 on the device (device forcing terms)."""
+    from paper_2601_02540_b200 import cli
+    from paper_2601_02540_b200.scenarios import make_scenario
+    spec = make_scenario("manufactured", {"bounded": bounded})
+    t = cli.run_convergence_study(spec, [32, 64, 128], H.IntegratorConfig(abs_tol=1e-10, rel_tol=1e-10))
+    assert t.status == ["ok"] * 3
+    assert all(1.8 < r < 2.2 for r in t.rates[-1]), t.rates
