@@ -402,7 +402,9 @@ __device__ __forceinline__ void neighbour_y(const double2* S, YQ& Y) {
 // rhs.hpp:212-213) at one node of row j.  S: ring slot of row j (centre at
 // S + tid, x-neighbours at S + sl / S + sr); ypr / ynr: the y-quantities of
 // rows j-1 / j+1 at this column.  All stage kernels share it.
-template <int KIND>
+// SW / SRC: the kernel may see rhs_shallow_water / a source term (the fused
+// fixed-step kernels never do: the host launches them only without either).
+template <int KIND, bool SW = true, bool SRC = true>
 __device__ __forceinline__ void tendency(const StageArgs& A, const double2* S, int tid, int sl, int sr, double cx,
                                          double cy, bool xl, bool xr, int i, int j, const YQ& ypr, const YQ& ynr,
                                          double rh, double o[5]) {
@@ -430,7 +432,9 @@ __device__ __forceinline__ void tendency(const StageArgs& A, const double2* S, i
     {  // continuity (rhs.hpp:156-157) + wall SAT (sbp.hpp:272-284)
         const double s = sc(dadd(dadd(dadd(dmul(u, dh_x), dmul(h, du_x)), dmul(v, dh_y)), dmul(h, dv_y)));
         double ht = -s;
-        if (A.walls) {
+        // KIND 2 implies no walls (host-checked); only the fused kernels
+        // compile the test out (the per-stage kernels measured slower without it)
+        if ((SRC || KIND != 2) && A.walls) {
             double sat = 0.0;
             if (xl) sat = dsub(sat, dmul(A.tdx, hu));
             if (xr) sat = dadd(sat, dmul(A.tdx, hu));
@@ -488,11 +492,11 @@ __device__ __forceinline__ void tendency(const StageArgs& A, const double2* S, i
             dadd(dadd(dadd(dmul(u, de_x), dmul(v, de_y)), dmul(dmul(1.5, u), db_x)), dmul(dmul(1.5, v), db_y));
         o[4] = dsub(w, sc(s));
     }
-    if (A.shallow) {  // rhs_shallow_water zeroes the decoupled tendencies
+    if (SW && A.shallow) {  // rhs_shallow_water zeroes the decoupled tendencies
         o[3] = 0.0;
         o[4] = 0.0;
     }
-    if (A.source) {  // add_manufactured_sources: after assembly (rhs.hpp:212-213)
+    if (SRC && A.source) {  // add_manufactured_sources: after assembly (rhs.hpp:212-213)
         const double xg = dadd(A.x_min, dmul((double)i, A.dx));
         const double yg = dadd(A.y_min, dmul((double)(A.j_global0 + j), A.dy));
         double s5[5];
@@ -792,7 +796,7 @@ __device__ __forceinline__ void s31_half3(const StageArgs& A, const KPtrs& P, Th
     neighbour_y(ap + T.tid, yp);
     const double cy = (r == T.jc0 || r == T.jc1) ? A.c1y : A.cpy;
     double o[5];
-    tendency<KIND>(A, ac, T.tid, T.sl, T.sr, T.cx, cy, T.xl, T.xr, T.i, r, yp, yn, rh, o);
+    tendency<KIND, false, false>(A, ac, T.tid, T.sl, T.sr, T.cx, cy, T.xl, T.xr, T.i, r, yp, yn, rh, o);
     const bool own = T.fb && r >= T.j0 && r < T.j1;
     if (own) {
         const unsigned off = (unsigned)(r + GHOST) * (unsigned)A.nx + T.col;
@@ -831,7 +835,7 @@ __device__ __forceinline__ void s31_half1(const StageArgs& A, const KPtrs& P, co
     const YQ& yn = hi ? yc : ynb;
     const double cy = (j == T.jc0 || j == T.jc1) ? A.c1y : A.cpy;
     double o[5];
-    tendency<KIND>(A, bc, T.tid, T.sl, T.sr, T.cx, cy, T.xl, T.xr, T.i, j, yp, yn, rh, o);
+    tendency<KIND, false, false>(A, bc, T.tid, T.sl, T.sr, T.cx, cy, T.xl, T.xr, T.i, j, yp, yn, rh, o);
     const unsigned off = (unsigned)(j + GHOST) * (unsigned)A.nx + T.col;
 #pragma unroll
     for (int f = 0; f < 5; ++f) P.out2[f][off] = o[f];
@@ -1005,20 +1009,23 @@ __global__ void __launch_bounds__(BX, HSGN_S12_MINB) sgn_s12_kernel(const StageA
         if (s_skip) return;
     }
     const int nx = A.nx, ny = A.ny;
+    // KIND 2 (common factor) is only chosen for fully periodic grids without
+    // walls (host-checked): the wall / clamp branches compile out
+    constexpr bool PER = KIND == 2;
     const int i = (int)blockIdx.x * WX2 - 2 + tid;
     const bool fa = tid >= 1 && tid <= BX - 2 && i >= -1 && i <= nx;  // stage-1 finish
     const bool fb = tid >= 2 && tid <= BX - 3 && i >= 0 && i < nx;    // stage-2 finish (owned column)
     int c = i;
-    if (i < 0) c = A.x_bounded ? 0 : nx + i;
-    if (i >= nx) c = (A.x_bounded || i > nx + 1) ? nx - 1 : i - nx;
+    if (i < 0) c = (!PER && A.x_bounded) ? 0 : nx + i;
+    if (i >= nx) c = ((!PER && A.x_bounded) || i > nx + 1) ? nx - 1 : i - nx;
     const unsigned col = (unsigned)c;
-    const bool xl = A.x_bounded && i == 0, xr = A.x_bounded && i == nx - 1;
+    const bool xl = !PER && A.x_bounded && i == 0, xr = !PER && A.x_bounded && i == nx - 1;
     const double cx = (xl || xr) ? A.c1x : A.cpx;
     const int sl = xl ? tid : tid - 1, sr = xr ? tid : tid + 1;
     const int j0 = A.band0 + blockIdx.y * A.rows_per_block;
     const int j1 = min(A.band1 > 0 ? A.band1 : ny, j0 + A.rows_per_block);
-    const int jc0 = A.y_lo == YE_CLAMP ? 0 : INT_MIN, jc1 = A.y_hi == YE_CLAMP ? ny - 1 : INT_MIN;
-    const bool clamp_hi = A.y_hi == YE_CLAMP;
+    const int jc0 = (!PER && A.y_lo == YE_CLAMP) ? 0 : INT_MIN, jc1 = (!PER && A.y_hi == YE_CLAMP) ? ny - 1 : INT_MIN;
+    const bool clamp_lo = !PER && A.y_lo == YE_CLAMP, clamp_hi = !PER && A.y_hi == YE_CLAMP;
     const unsigned unx = (unsigned)nx;
     unsigned long long bad1 = 0, bad2 = 0, my_min = ~0ull;
 
@@ -1059,12 +1066,12 @@ __global__ void __launch_bounds__(BX, HSGN_S12_MINB) sgn_s12_kernel(const StageA
                 kj[f] = __ldg(P.k[f] + offj);
             }
             YQ yp, yc;
-            ywin_prev(A, j, pa, pb, tid, yp);
+            neighbour_y((clamp_lo && j == 0 ? pb : pa) + tid, yp);  // ywin_prev
             const bool hi = clamp_hi && j == ny - 1;
             if (hi || !HSGN_S12_PASS_A) neighbour_y((hi ? pb : pc) + tid, yc);
             const double cy = (j == jc0 || j == jc1) ? A.c1y : A.cpy;
             double k2[5];
-            tendency<KIND>(A, pb, tid, sl, sr, cx, cy, xl, xr, i, j, yp, (hi || !HSGN_S12_PASS_A) ? yc : ya, rhap,
+            tendency<KIND, false, false>(A, pb, tid, sl, sr, cx, cy, xl, xr, i, j, yp, (hi || !HSGN_S12_PASS_A) ? yc : ya, rhap,
                            k2);
             double q[5];
 #pragma unroll
@@ -1085,7 +1092,7 @@ __global__ void __launch_bounds__(BX, HSGN_S12_MINB) sgn_s12_kernel(const StageA
         if (r - 2 >= j0 && fb) {
             const int j = r - 2;
             YQ yp, yc;
-            ywin_prev(A, j, qa, qb, tid, yp);
+            neighbour_y((clamp_lo && j == 0 ? qb : qa) + tid, yp);  // ywin_prev
             const bool hi = clamp_hi && j == ny - 1;
             if (hi) neighbour_y(qb + tid, yc);
             const double cy = (j == jc0 || j == jc1) ? A.c1y : A.cpy;
@@ -1096,7 +1103,7 @@ __global__ void __launch_bounds__(BX, HSGN_S12_MINB) sgn_s12_kernel(const StageA
                 for (int f = 0; f < 5; ++f) e12[f] = P.part[f][off];
             }
             double k3[5];
-            tendency<KIND>(A, qb, tid, sl, sr, cx, cy, xl, xr, i, j, yp, hi ? yc : yb, rhbp, k3);
+            tendency<KIND, false, false>(A, qb, tid, sl, sr, cx, cy, xl, xr, i, j, yp, hi ? yc : yb, rhbp, k3);
 #pragma unroll
             for (int f = 0; f < 5; ++f) P.out[f][off] = dadd(partp[f], dmul(A.c3, k3[f]));  // state_add3
             if (ADAPT) {  // ((d1 k1 + d2 k2) + d3 k3) (time_integration.hpp:128-129)
@@ -1241,7 +1248,7 @@ __global__ void __launch_bounds__(BX, HSGN_STEP_MINB) sgn_step_kernel(const Stag
             neighbour_y((clamp_hi && j == ny - 1 ? p1b : p1c) + tid, yn);
             const double cy = (j == jc0 || j == jc1) ? A.c1y : A.cpy;
             double k2[5];
-            tendency<KIND>(A, p1b, tid, sl, sr, cx, cy, xl, xr, i, j, yp, yn, rh1p, k2);
+            tendency<KIND, false, false>(A, p1b, tid, sl, sr, cx, cy, xl, xr, i, j, yp, yn, rh1p, k2);
             double q[5];
 #pragma unroll
             for (int f = 0; f < 5; ++f) {
@@ -1262,7 +1269,7 @@ __global__ void __launch_bounds__(BX, HSGN_STEP_MINB) sgn_step_kernel(const Stag
             neighbour_y((clamp_hi && j == ny - 1 ? p2b : p2c) + tid, yn);
             const double cy = (j == jc0 || j == jc1) ? A.c1y : A.cpy;
             double k3[5];
-            tendency<KIND>(A, p2b, tid, sl, sr, cx, cy, xl, xr, i, j, yp, yn, rh2p, k3);
+            tendency<KIND, false, false>(A, p2b, tid, sl, sr, cx, cy, xl, xr, i, j, yp, yn, rh2p, k3);
             double ynw[5];
 #pragma unroll
             for (int f = 0; f < 5; ++f) ynw[f] = dadd(partp[f], dmul(A.c3, k3[f]));  // state_add3
@@ -1287,7 +1294,7 @@ __global__ void __launch_bounds__(BX, HSGN_STEP_MINB) sgn_step_kernel(const Stag
             if (hi) neighbour_y(p3b + tid, yc);
             const double cy = (j == jc0 || j == jc1) ? A.c1y : A.cpy;
             double k4[5];
-            tendency<KIND>(A, p3b, tid, sl, sr, cx, cy, xl, xr, i, j, yp, hi ? yc : y3, rh3p, k4);
+            tendency<KIND, false, false>(A, p3b, tid, sl, sr, cx, cy, xl, xr, i, j, yp, hi ? yc : y3, rh3p, k4);
             const unsigned off = (unsigned)(j + GHOST) * unx + col;
 #pragma unroll
             for (int f = 0; f < 5; ++f) P.out2[f][off] = k4[f];
@@ -1411,6 +1418,7 @@ static cudaError_t launch_mode(const StageArgs& A, cudaStream_t st) {
 
 template <int KIND>
 static cudaError_t launch_s31(const StageArgs& A, cudaStream_t st) {
+    if (A.source || A.shallow) return cudaErrorInvalidValue;  // fused kernels: neither (see tendency)
     constexpr size_t bytes = sizeof(double2) * 2 * 3 * NPF * BX;
     static unsigned long long opted = 0;
     const cudaError_t e = smem_opt_in(opted, sgn_s31_kernel<KIND>, bytes);
@@ -1432,6 +1440,7 @@ static cudaError_t launch_s31(const StageArgs& A, cudaStream_t st) {
 
 template <int KIND>
 static cudaError_t launch_step(const StageArgs& A, cudaStream_t st) {
+    if (A.source || A.shallow) return cudaErrorInvalidValue;  // fused kernels: neither (see tendency)
     constexpr size_t bytes = sizeof(double2) * 3 * 3 * NPF * BX;
     static unsigned long long opted = 0;
     const cudaError_t e = smem_opt_in(opted, sgn_step_kernel<KIND>, bytes);
@@ -1454,6 +1463,7 @@ static cudaError_t launch_step(const StageArgs& A, cudaStream_t st) {
 
 template <int KIND>
 static cudaError_t launch_s12(const StageArgs& A, cudaStream_t st) {
+    if (A.source || A.shallow) return cudaErrorInvalidValue;  // fused kernels: neither (see tendency)
     constexpr size_t bytes = sizeof(double2) * 2 * 3 * NPF * BX;
     static unsigned long long opted_f = 0, opted_a = 0;
     cudaError_t e = smem_opt_in(opted_f, sgn_s12_kernel<KIND, false>, bytes);
