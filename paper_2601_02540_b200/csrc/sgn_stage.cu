@@ -47,6 +47,9 @@ constexpr int WX = BX - 2;  // finished columns per tile
 
 template <int MODE>
 __host__ __device__ constexpr int npairs() { return MODE == MODE_S2 ? NPAIRS_S2 : NPAIRS; }
+#ifndef HSGN_RCP_NOBRANCH
+#define HSGN_RCP_NOBRANCH 1  // rcp_or_nan (sgn_device.cuh) instead of __drcp_rn
+#endif
 #ifndef HSGN_S3_WARPS
 #define HSGN_S3_WARPS 20  // resident warps per SM asked of the fixed-step stage-3 kernel
 #endif
@@ -116,7 +119,7 @@ template <bool STORE_RH = true>
 __device__ __forceinline__ bool products_q(const double q[5], double b, double2* S, YQ& Y, double* rh_out) {
     const double h = q[0], u = q[1], v = q[2], w = q[3], e = q[4];
     const bool ok = h > 0.0;
-    const double rh = __drcp_rn(h);
+    const double rh = HSGN_RCP_NOBRANCH ? rcp_or_nan(h) : __drcp_rn(h);
     bool slow = false;
     double r = div_fast(e, h, rh, slow);  // eta/h computed once (rhs.hpp:86-88)
     if (slow) r = e / h;
@@ -981,6 +984,10 @@ __device__ __forceinline__ void ywin_prev(const StageArgs& A, int j, const doubl
 #ifndef HSGN_S12_PASS_A
 #define HSGN_S12_PASS_A 1
 #endif
+#ifndef HSGN_S12_UNROLL
+#define HSGN_S12_UNROLL 1  // march unroll of S12 (1: one copy of the loop body in the I-cache)
+#endif
+constexpr int kS12Unroll = HSGN_S12_UNROLL;
 #ifndef HSGN_S12_LATE_PF
 #define HSGN_S12_LATE_PF 0
 #endif
@@ -1041,7 +1048,7 @@ __global__ void __launch_bounds__(BX, HSGN_S12_MINB) sgn_s12_kernel(const StageA
 
     Raw raw;
     load_raw<MODE_S1>(P, (unsigned)map_row2(A, j0 - 2) * unx + col, raw);
-#pragma unroll 1
+#pragma unroll kS12Unroll
     for (int r = j0 - 2; r <= j1 + 1; ++r) {
         // ---- P1: stage-1 input of row r (raw of row r+1 loaded right after)
         YQ ya;
