@@ -42,8 +42,8 @@ BYTES_PER_NODE = {"S1": 128, "S2": 168, "S3": 88, "S31": 128, "STEP": 168, "S12"
 BYTES_PER_POINT_STAGE = 128  # unfused step: 384 B per node / 3 stages
 # FP64 instructions (DADD + DMUL + DFMA) per node of each kernel, from the ncu
 # SASS mixes in profiles/ (r1_sass_mix_stage_kernels.txt, r1f_sass_mix_s31.txt,
-# r1g_sass_mix_s12.txt): the compute roofline of the FP64-issue-bound kernels
-FP64_PER_NODE = {"S1": 199.5, "S2": 228.8, "S3": 189.1, "S31": 397.3, "S12": 439.6}
+# r1j_sass_mix_s12.txt, r1j_sass_mix_s3.txt): the compute roofline of the FP64-issue-bound kernels
+FP64_PER_NODE = {"S1": 199.5, "S2": 228.8, "S3": 189.1, "S31": 397.3, "S12": 437.5}
 FP64_LANES_PER_SM, N_SM = 64, 148
 
 
