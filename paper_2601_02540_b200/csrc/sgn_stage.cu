@@ -256,6 +256,9 @@ __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)_
 __device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
@@ -984,6 +987,9 @@ __device__ __forceinline__ void ywin_prev(const StageArgs& A, int j, const doubl
 #ifndef HSGN_S12_PASS_A
 #define HSGN_S12_PASS_A 1
 #endif
+#ifndef HSGN_S12_SPLITBAR
+#define HSGN_S12_SPLITBAR 1  // split-phase row barrier (mbarrier arrive after H2, wait after the next P1)
+#endif
 #ifndef HSGN_S12_UNROLL
 #define HSGN_S12_UNROLL 1  // march unroll of S12 (1: one copy of the loop body in the I-cache)
 #endif
@@ -1046,10 +1052,27 @@ __global__ void __launch_bounds__(BX, HSGN_S12_MINB) sgn_s12_kernel(const StageA
 #pragma unroll
     for (int f = 0; f < 5; ++f) partp[f] = 0.0;
 
+    // Split-phase row barrier (HSGN_S12_SPLITBAR): iteration k arrives on
+    // s_bar[k & 1] after its H2 and iteration k + 1 waits for that phase only
+    // after its P1.  P1(r) needs no wait of its own (it overwrites ring A row
+    // r-3, last read across threads in iteration k - 2), so a warp that is
+    // ahead forms the next stage-1 input while the others finish.
+    // (Measured slower: a second barrier set -- arrive after P1 / wait before
+    // H1, arrive after H1 / wait before H2 -- with a 4-slot ring B, 2.68 vs
+    // 2.63 ms.)
+    __shared__ __align__(8) unsigned long long s_bar[2];
+    if (HSGN_S12_SPLITBAR) {
+        if (tid == 0) {
+            for (int q = 0; q < 2; ++q) mbar_init(&s_bar[q], BX);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();
+    }
     Raw raw;
     load_raw<MODE_S1>(P, (unsigned)map_row2(A, j0 - 2) * unx + col, raw);
+    int k = 0;  // iteration index (split barrier phases)
 #pragma unroll kS12Unroll
-    for (int r = j0 - 2; r <= j1 + 1; ++r) {
+    for (int r = j0 - 2; r <= j1 + 1; ++r, ++k) {
         // ---- P1: stage-1 input of row r (raw of row r+1 loaded right after)
         YQ ya;
         double rhac;
@@ -1058,7 +1081,11 @@ __global__ void __launch_bounds__(BX, HSGN_S12_MINB) sgn_s12_kernel(const StageA
             if (fb && r >= j0 && r < j1 && !ok) ++bad1;
         }
         if (!HSGN_S12_LATE_PF && r + 1 <= j1 + 1) load_raw<MODE_S1>(P, (unsigned)map_row2(A, r + 1) * unx + col, raw);
-        __syncthreads();
+        if (HSGN_S12_SPLITBAR) {
+            if (k > 0) mbar_wait(&s_bar[(k - 1) & 1], (unsigned)((k - 1) >> 1) & 1u);
+        } else {
+            __syncthreads();
+        }
         // ---- H1: k2 at row r-1 -> stage-2 input -> ring B (qc)
         YQ yb;
         double rhbc = 0.0, partc[5];
@@ -1121,6 +1148,7 @@ __global__ void __launch_bounds__(BX, HSGN_S12_MINB) sgn_s12_kernel(const StageA
                 (unsigned long long)__double_as_longlong(dadd(partp[0], dmul(A.c3, k3[0])));
             my_min = bits < my_min ? bits : my_min;
         }
+        if (HSGN_S12_SPLITBAR) mbar_arrive(&s_bar[k & 1]);
         // ---- rotate
         double2* t = pa;
         pa = pb;
