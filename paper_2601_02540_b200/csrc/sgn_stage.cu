@@ -385,6 +385,22 @@ __device__ __forceinline__ void neighbour_x(const double2* S, XQ& X) {
 #ifndef HSGN_YWIN_SMEM
 #define HSGN_YWIN_SMEM 1
 #endif
+#ifndef HSGN_STAGE_SPLITBAR
+#define HSGN_STAGE_SPLITBAR 1
+#endif
+// Split-phase row barrier of the stage-3 kernels (measured: S3 1.235 ->
+// 1.219 ms; S1 1.447 -> 1.478, so S1 / RHS keep __syncthreads), as in S12: step j
+// arrives on an mbarrier after finishing row j and the next step waits for
+// that phase only after forming its next row's products, so a warp that is
+// ahead does that work instead of idling at the barrier.  (A 4-slot ring
+// with the arrive right after the products -- a whole step of slack --
+// measured far slower: 40 KB rings squeeze L1.)
+template <int MODE, bool TMA>
+__host__ __device__ constexpr bool split_bar() {
+    return HSGN_STAGE_SPLITBAR && !TMA && HSGN_YWIN_SMEM && (MODE == MODE_S3 || MODE == MODE_S3A);
+}
+template <int MODE, bool TMA>
+__host__ __device__ constexpr int ring_slots() { return 3; }
 
 // y-quantities of a row re-formed from its own-column ring pairs (same
 // operations as products(), so bit-identical to the carried values).
@@ -517,9 +533,11 @@ __device__ __forceinline__ void tendency(const StageArgs& A, const double2* S, i
 template <int MODE, int KIND, bool TMA, int SC>
 __device__ __forceinline__ void march_row(const StageArgs& A, const KPtrs& P, Thr& T, double2* ring, double* rawring,
                                           unsigned long long* bars, int j0, int j, const YQ& yp, YQ& yn, Raw& raw,
-                                          Raw& raw_next) {
+                                          Raw& raw_next, unsigned long long* sbar) {
     constexpr int NP = npairs<MODE>();
-    constexpr int SN = (SC + 1) % 3;
+    constexpr int NS = ring_slots<MODE, TMA>();
+    constexpr bool SPLIT = split_bar<MODE, TMA>();
+    constexpr int SN = (SC + 1) % NS;
     const int jn = j + 1;
     const unsigned nx = (unsigned)A.nx;
     // register prefetch of raw(jn+1), issued after products(jn) so the load is
@@ -546,8 +564,16 @@ __device__ __forceinline__ void march_row(const StageArgs& A, const KPtrs& P, Th
     // One barrier per row: row j's ring entries (written one step ago) become
     // visible, and this step's writes to slot SN are ordered after the last
     // reads of that slot (finish of row j-2, before the previous barrier).
-    __syncthreads();
-    if (!T.finish) return;
+    const int t = j - j0 + 1;  // step index (the prologue is step 0)
+    if (SPLIT) {
+        mbar_wait(&sbar[(t - 1) & 1], (unsigned)((t - 1) >> 1) & 1u);
+    } else {
+        __syncthreads();
+    }
+    if (!T.finish) {
+        if (SPLIT) mbar_arrive(&sbar[t & 1]);
+        return;
+    }
 
     const double2* S = ring + SC * (NP * BX);
     const double2* Sc = S + T.tid;  // row j, own column
@@ -558,7 +584,7 @@ __device__ __forceinline__ void march_row(const StageArgs& A, const KPtrs& P, Th
     // (measured faster for S2, r1: 2.05 vs 2.95 ms).
     constexpr bool ywin_smem = HSGN_YWIN_SMEM && MODE != MODE_S2;
     YQ yprev;
-    if (ywin_smem) neighbour_y(ring + ((SC + 2) % 3) * (NP * BX) + T.tid, yprev);
+    if (ywin_smem) neighbour_y(ring + ((SC + NS - 1) % NS) * (NP * BX) + T.tid, yprev);
     const YQ& ypr = ywin_smem ? yprev : yp;
     const unsigned off = (unsigned)(j + 1) * nx + T.col;  // bases point at row -1
     // S3A: the error-norm inputs of this node are requested before the
@@ -607,6 +633,7 @@ __device__ __forceinline__ void march_row(const StageArgs& A, const KPtrs& P, Th
             T.my_err = dadd(T.my_err, acc);
         }
     }
+    if (SPLIT) mbar_arrive(&sbar[t & 1]);  // row j finished: its slot may be reused after the next wait
 }
 
 template <int MODE, int KIND, bool TMA>
@@ -694,7 +721,8 @@ __global__ void __launch_bounds__(BX, min_blocks<MODE>()) sgn_stage_kernel(const
     } else {
         load_raw<MODE>(P, (unsigned)map_row(A, j0 - 1) * unx + T.col, raw);
     }
-    products<MODE>(A, raw, ring + 2 * (NP * BX) + tid, yc);
+    constexpr int NS = ring_slots<MODE, TMA>();
+    products<MODE>(A, raw, ring + (NS - 1) * (NP * BX) + tid, yc);
     if (TMA) {
         mbar_wait(&bars[1], 0);
         raw_from_smem<MODE>(rawring + nraw<MODE>() * RW, tid, raw);
@@ -716,12 +744,22 @@ __global__ void __launch_bounds__(BX, min_blocks<MODE>()) sgn_stage_kernel(const
     // ---- march, unrolled by 3: row j lives in ring slot (j-j0)%3 and register
     // set {a,b,c}[(j-j0)%3]; step SC reads set SC+2 (row j-1), writes SC+1.
     Raw raw2;  // next-row prefetch target when it overlaps products (EARLY)
+    __shared__ __align__(8) unsigned long long sbar[2];
+    if (split_bar<MODE, TMA>()) {
+        if (tid == 0) {
+            mbar_init(&sbar[0], BX);
+            mbar_init(&sbar[1], BX);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();
+        mbar_arrive(&sbar[0]);  // step 0: rows j0-1 and j0 written
+    }
     for (int j = j0; j < T.j1; j += 3) {
-        march_row<MODE, KIND, TMA, 0>(A, P, T, ring, rawring, bars, j0, j, yc, yb, raw, raw2);
+        march_row<MODE, KIND, TMA, 0>(A, P, T, ring, rawring, bars, j0, j, yc, yb, raw, raw2, sbar);
         if (j + 1 >= T.j1) break;
-        march_row<MODE, KIND, TMA, 1>(A, P, T, ring, rawring, bars, j0, j + 1, ya, yc, raw, raw2);
+        march_row<MODE, KIND, TMA, 1>(A, P, T, ring, rawring, bars, j0, j + 1, ya, yc, raw, raw2, sbar);
         if (j + 2 >= T.j1) break;
-        march_row<MODE, KIND, TMA, 2>(A, P, T, ring, rawring, bars, j0, j + 2, yb, ya, raw, raw2);
+        march_row<MODE, KIND, TMA, 2>(A, P, T, ring, rawring, bars, j0, j + 2, yb, ya, raw, raw2, sbar);
     }
 
     // ---- block reductions (fixed order inside the block)
@@ -1405,7 +1443,8 @@ __host__ __device__ constexpr size_t ring_bytes() {
     // (S2 must keep ~80 KB of L1 beside its rings -- 3 CTAs of 49 KB: its 16
     // misaligned raw streams rely on L1 line reuse between neighbouring warps;
     // at 4 CTAs or with padded rings it measured 2.95 vs 2.05 ms at 8192^2.)
-    return sizeof(double2) * 3 * npairs<MODE>() * BX + (TMA ? sizeof(double) * RSLOTS * nraw<MODE>() * RW : 0);
+    return sizeof(double2) * ring_slots<MODE, TMA>() * npairs<MODE>() * BX +
+           (TMA ? sizeof(double) * RSLOTS * nraw<MODE>() * RW : 0);
 }
 
 // Dynamic shared memory above the 48 KB default needs a per-function opt-in,
