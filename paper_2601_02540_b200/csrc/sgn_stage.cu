@@ -1028,6 +1028,9 @@ __device__ __forceinline__ void ywin_prev(const StageArgs& A, int j, const doubl
 #ifndef HSGN_S12_SPLITBAR
 #define HSGN_S12_SPLITBAR 1  // split-phase row barrier (mbarrier arrive after H2, wait after the next P1)
 #endif
+#ifndef HSGN_S12_EARLY_H1
+#define HSGN_S12_EARLY_H1 1
+#endif
 #ifndef HSGN_S12_UNROLL
 #define HSGN_S12_UNROLL 1  // march unroll of S12 (1: one copy of the loop body in the I-cache)
 #endif
@@ -1119,6 +1122,21 @@ __global__ void __launch_bounds__(BX, HSGN_S12_MINB) sgn_s12_kernel(const StageA
             if (fb && r >= j0 && r < j1 && !ok) ++bad1;
         }
         if (!HSGN_S12_LATE_PF && r + 1 <= j1 + 1) load_raw<MODE_S1>(P, (unsigned)map_row2(A, r + 1) * unx + col, raw);
+        // H1's own-column inputs need no barrier: with the split barrier they
+        // are requested before the wait (HSGN_S12_EARLY_H1: 1 the reloads,
+        // 2 also the y-window of row r-2)
+        const bool do1 = r - 1 >= j0 - 1 && fa;
+        double yj[5], kj[5];
+        YQ yp1;
+        if (HSGN_S12_EARLY_H1 >= 1 && do1) {
+            const unsigned offj = (unsigned)map_row2(A, r - 1) * unx + col;
+#pragma unroll
+            for (int f = 0; f < 5; ++f) {
+                yj[f] = __ldg(P.y[f] + offj);
+                kj[f] = __ldg(P.k[f] + offj);
+            }
+            if (HSGN_S12_EARLY_H1 >= 2) neighbour_y((clamp_lo && r - 1 == 0 ? pb : pa) + tid, yp1);
+        }
         if (HSGN_S12_SPLITBAR) {
             if (k > 0) mbar_wait(&s_bar[(k - 1) & 1], (unsigned)((k - 1) >> 1) & 1u);
         } else {
@@ -1127,18 +1145,22 @@ __global__ void __launch_bounds__(BX, HSGN_S12_MINB) sgn_s12_kernel(const StageA
         // ---- H1: k2 at row r-1 -> stage-2 input -> ring B (qc)
         YQ yb;
         double rhbc = 0.0, partc[5];
-        if (r - 1 >= j0 - 1 && fa) {
+        if (do1) {
             const int j = r - 1;
             // y, k1 of row j again (this thread loaded them one row ago: L1/L2)
             const unsigned offj = (unsigned)map_row2(A, j) * unx + col;
-            double yj[5], kj[5];
+            if (HSGN_S12_EARLY_H1 < 1) {
 #pragma unroll
-            for (int f = 0; f < 5; ++f) {
-                yj[f] = __ldg(P.y[f] + offj);
-                kj[f] = __ldg(P.k[f] + offj);
+                for (int f = 0; f < 5; ++f) {
+                    yj[f] = __ldg(P.y[f] + offj);
+                    kj[f] = __ldg(P.k[f] + offj);
+                }
             }
             YQ yp, yc;
-            neighbour_y((clamp_lo && j == 0 ? pb : pa) + tid, yp);  // ywin_prev
+            if (HSGN_S12_EARLY_H1 >= 2)
+                yp = yp1;
+            else
+                neighbour_y((clamp_lo && j == 0 ? pb : pa) + tid, yp);  // ywin_prev
             const bool hi = clamp_hi && j == ny - 1;
             if (hi || !HSGN_S12_PASS_A) neighbour_y((hi ? pb : pc) + tid, yc);
             const double cy = (j == jc0 || j == jc1) ? A.c1y : A.cpy;
