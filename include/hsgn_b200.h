@@ -207,6 +207,10 @@ hsgn_status hsgn_recorder_snapshot(const hsgn_recorder* r, int32_t k, double* ta
  * if any stage input had !(h > 0); *steps_done gets the completed count. */
 hsgn_status hsgn_bs3_fixed_steps(hsgn_ctx* ctx, hsgn_state* y, hsgn_state* k1, double t, double dt,
                                  int64_t steps, int64_t* steps_done);
+/* Builds (captures and instantiates) the CUDA graphs that
+ * hsgn_bs3_fixed_steps(ctx, ..., dt, steps, ...) will launch, without running
+ * a step: graph construction is one-time host work, kept out of a timed run. */
+hsgn_status hsgn_prepare_fixed_steps(hsgn_ctx* ctx, double dt, int64_t steps);
 
 /* ------------------------------------------------------------ diagnostics */
 

@@ -101,6 +101,7 @@ def lib() -> C.CDLL:
     f("hsgn_init_auxiliary", C.c_int, CTX, STATE)
     f("hsgn_solve", C.c_int, CTX, STATE, D, D, CF, STATE, RC, OBSERVER, C.c_void_p)
     f("hsgn_bs3_fixed_steps", C.c_int, CTX, STATE, STATE, D, D, I64, C.POINTER(I64))
+    f("hsgn_prepare_fixed_steps", C.c_int, CTX, D, I64)
     f("hsgn_total_mass", C.c_int, CTX, STATE, PD)
     f("hsgn_total_energy", C.c_int, CTX, STATE, PD)
     f("hsgn_energy_rate", C.c_int, CTX, STATE, STATE, PD)
@@ -159,5 +160,5 @@ EXPORTS = [
     "hsgn_recorder_gauge_node", "hsgn_recorder_gauges", "hsgn_recorder_conservation", "hsgn_recorder_snapshot",
     "hsgn_set_fused_stages", "hsgn_fused_stages", "hsgn_profile_fused",
     "hsgn_scenario_count", "hsgn_scenario_name", "hsgn_scenario_make", "hsgn_scenario_sample",
-    "hsgn_scenario_exact",
+    "hsgn_scenario_exact", "hsgn_prepare_fixed_steps",
 ]

@@ -477,6 +477,12 @@ def adaptive_solve(ctx: RhsContext, q0, t0: float, t_final: float, cfg: Integrat
     return res
 
 
+def prepare_fixed_steps(ctx: RhsContext, dt: float, steps: int) -> None:
+    """Build the CUDA graphs bs3_fixed_steps(ctx, ..., dt, steps) will launch
+    (one-time host work; no step is run)."""
+    _check(ctx, N.lib().hsgn_prepare_fixed_steps(ctx._h, float(dt), int(steps)), "prepare_fixed_steps")
+
+
 def bs3_fixed_steps(ctx: RhsContext, y: DeviceState, k1: DeviceState, t: float, dt: float, steps: int):
     """The bare fused fixed-step pipeline (benchmark entry): returns
     (steps_done, device_ms, kernels)."""

@@ -1723,6 +1723,24 @@ extern "C" hsgn_status hsgn_recorder_snapshot(const hsgn_recorder* R, int32_t k,
     return HSGN_OK;
 }
 
+extern "C" hsgn_status hsgn_prepare_fixed_steps(hsgn_ctx* c, double dt, int64_t steps) {
+    if (!c || steps < 0) return HSGN_EINVAL;
+    DeviceGuard dg_(c->device);
+    const int CHUNK = 64;  // the chunking of hsgn_bs3_fixed_steps (even chunks keep buffer parity 0)
+    hsgn_status st;
+    if ((st = ensure_ws(c, CHUNK))) return st;
+    if (!whole(c) || c->source) return HSGN_OK;  // direct launches: nothing to build
+    c->base.h_floor = c->phys.h_floor;
+    for (int64_t left = steps; left > 1;) {
+        int n = (int)std::min<int64_t>(CHUNK, left);
+        if (n & 1) --n;
+        FixedGraph* fg = nullptr;
+        if ((st = get_fixed_graph(c, n, 0, dt, nullptr, &fg))) return st;
+        left -= n;
+    }
+    return HSGN_OK;
+}
+
 extern "C" hsgn_status hsgn_bs3_fixed_steps(hsgn_ctx* c, hsgn_state* y, hsgn_state* k1, double t, double dt,
                                             int64_t steps, int64_t* steps_done) {
     if (!c || !y || !k1 || steps < 0) return HSGN_EINVAL;
