@@ -197,3 +197,37 @@ def test_adaptive_solve_matches_reference_closely(orc):
         assert not res.aborted and res.t == rec.t
         assert abs(res.accepted - rec.accepted) <= 1 and res.rhs_evals_setup == rec.rhs_evals_setup
         assert np.max(np.abs(res.q.flat() - want)) <= 1e-9 * np.max(np.abs(want))
+
+
+def test_config3_full_4096_long_time(tmp_path):
+    """BASELINE config 3 at its stated size: the reflecting basin
+    (gaussian_obstacle, walls on all four sides, variable bathymetry) on a
+    4096 x 4096 grid, 3000 fixed steps through the CLI path (scenario
+    registry + on-device recorder, a conservation row every 250 steps).
+    Mass is a linear invariant of the scheme: drift <= 1e-12 relative over
+    the whole run.  The semidiscrete energy rate is round-off: |dE/dt| <=
+    1e-11 E at every record.  The fully discrete energy drift is the BS3
+    time-integration error (small, not round-off)."""
+    from paper_2601_02540_b200 import cli
+    from paper_2601_02540_b200.config import RunConfig
+    spec_dt = 0.5 * (20.0 / 4095) / (np.sqrt(9.81 * 0.3) + np.sqrt(500.0 / 3) + 1.0)
+    cfg = RunConfig(scenario="gaussian_obstacle", scenario_params={"bounded": 1.0}, nx=4096, ny=4096,
+                    t_final=3000 * spec_dt, output_dir=str(tmp_path / "basin"), conservation_stride=250,
+                    gauges_set=True, gauges=[(0.0, 0.0)], snapshots_set=True, snapshot_times=[])
+    cfg.integrator.fixed_dt = spec_dt
+    import io
+    log = io.StringIO()
+    assert cli.cmd_run(cfg, log) == 0, log.getvalue()
+    import json
+    meta = json.load(open(tmp_path / "basin" / "run_meta.json"))
+    assert meta["status"] == "ok" and meta["grid"]["nx"] == 4096 and meta["grid"]["boundary_y"] == "reflecting"
+    assert meta["steps"]["accepted"] >= 2999
+    assert abs(meta["conservation"]["mass_drift_rel"]) <= 1e-12
+    assert abs(meta["conservation"]["energy_drift_rel"]) <= 1e-6
+    rows = [ln.split(",") for ln in open(tmp_path / "basin" / "conservation.csv").read().splitlines()[1:]]
+    cons = np.array([[float(x) for x in r] for r in rows])
+    assert len(cons) >= 12
+    print("config3 4096^2:", meta["steps"], meta["conservation"], "max |rate|/E",
+          float(np.max(np.abs(cons[:, 3]) / np.abs(cons[:, 2]))), "wall", meta["wall_seconds"])
+    assert np.all(np.abs(cons[:, 1] - cons[0, 1]) <= 1e-12 * abs(cons[0, 1]))
+    assert np.all(np.abs(cons[:, 3]) <= 1e-11 * np.abs(cons[:, 2]))
