@@ -21,6 +21,7 @@
 #pragma once
 
 #include <array>
+#include <map>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -479,6 +480,98 @@ inline SolutionRecord adaptive_solve(RhsContext& ctx, const StateField& q0, doub
                                      const IntegratorConfig& cfg, RunRecorder& recorder,
                                      const AcceptObserver& on_accept = {}) {
     return detail::solve(ctx, q0, t0, t_final, cfg, on_accept, &recorder);
+}
+
+// ------------------------------------------------------------ scenarios
+// make_scenario / scenario_names / prepare_run / study exact solutions
+// (scenarios.hpp:18-707) over the native registry: the initial b, h, u, v are
+// sampled on the host bit-identically to the reference; w and eta come from
+// the device init_auxiliary, as prepare_run does.
+struct ScenarioSpec {
+    std::string name;
+    double x_min = 0, x_max = 1, y_min = 0, y_max = 1;
+    int nx_default = 64, ny_default = 64;
+    BoundaryKind kind_x = BoundaryKind::periodic, kind_y = BoundaryKind::periodic;
+    double g = 9.81, lambda = 500.0, t0 = 0.0, t_final = 1.0;
+    bool has_source = false, has_exact = false;
+    std::vector<std::string> exact_vars;
+    std::vector<std::array<double, 2>> gauges;
+    std::vector<double> snapshot_times;
+    hsgn_scenario native{};
+};
+
+inline std::vector<std::string> scenario_names() {
+    std::vector<std::string> out;
+    for (int k = 0; k < hsgn_scenario_count(); ++k) out.emplace_back(hsgn_scenario_name(k));
+    return out;
+}
+
+inline ScenarioSpec make_scenario(const std::string& name, const std::map<std::string, double>& params = {}) {
+    std::vector<const char*> keys;
+    std::vector<double> vals;
+    for (const auto& kv : params) {
+        keys.push_back(kv.first.c_str());
+        vals.push_back(kv.second);
+    }
+    ScenarioSpec s;
+    char err[256] = {0};
+    if (hsgn_scenario_make(name.c_str(), keys.data(), vals.data(), static_cast<int32_t>(keys.size()), &s.native,
+                           err, sizeof err) != HSGN_OK)
+        throw std::invalid_argument(err);  // scenarios.hpp:604-615, 697
+    const hsgn_scenario& c = s.native;
+    s.name = c.name;
+    s.x_min = c.domain.x_min;
+    s.x_max = c.domain.x_max;
+    s.y_min = c.domain.y_min;
+    s.y_max = c.domain.y_max;
+    s.nx_default = c.domain.nx;
+    s.ny_default = c.domain.ny;
+    s.kind_x = c.domain.kind_x ? BoundaryKind::bounded : BoundaryKind::periodic;
+    s.kind_y = c.domain.kind_y ? BoundaryKind::bounded : BoundaryKind::periodic;
+    s.g = c.g;
+    s.lambda = c.lambda;
+    s.t0 = c.t0;
+    s.t_final = c.t_final;
+    s.has_source = c.has_source != 0;
+    s.has_exact = c.has_exact != 0;
+    for (int k = 0; k < c.n_exact_vars; ++k) s.exact_vars.emplace_back(StateField::names()[c.exact_vars[k]]);
+    for (int k = 0; k < c.n_gauges; ++k) s.gauges.push_back({c.gauges[k][0], c.gauges[k][1]});
+    for (int k = 0; k < c.n_snapshots; ++k) s.snapshot_times.push_back(c.snapshot_times[k]);
+    return s;
+}
+
+// PreparedRun (scenarios.hpp:49-53): grid, device context (with the
+// manufactured forcing when the scenario has one) and q0.
+struct PreparedRun {
+    Grid2D grid;
+    RhsContext ctx;
+    StateField q0;
+};
+
+inline PreparedRun prepare_run(const ScenarioSpec& spec, int nx = 0, int ny = 0) {
+    nx = nx > 0 ? nx : spec.nx_default;
+    ny = ny > 0 ? ny : spec.ny_default;
+    const Grid2D grid = make_grid(spec.x_min, spec.x_max, spec.y_min, spec.y_max, nx, ny, spec.kind_x, spec.kind_y);
+    PhysSetup phys;
+    phys.g = spec.g;
+    phys.lambda = spec.lambda;
+    phys.b = Field2D(nx, ny);
+    std::vector<double> q(5 * grid.n_total());
+    if (hsgn_scenario_sample(&spec.native, nx, ny, phys.b.data(), q.data()) != HSGN_OK)
+        throw std::invalid_argument("prepare_run: sampling failed");
+    PreparedRun run{grid, RhsContext(grid, phys), StateField(grid)};
+    if (spec.has_source) run.ctx.set_manufactured_source(true);
+    detail::unpack(q, run.q0);
+    init_auxiliary(run.ctx, run.q0);  // model.hpp:93-105 on the device
+    return run;
+}
+
+// spec.exact (scenarios.hpp:155-170, 200-214)
+inline void exact_state(const ScenarioSpec& spec, double t, const Grid2D& grid, StateField& out) {
+    std::vector<double> q(5 * grid.n_total());
+    if (hsgn_scenario_exact(&spec.native, grid.nx, grid.ny, t, q.data()) != HSGN_OK)
+        throw std::invalid_argument("scenario '" + spec.name + "' has no exact solution");
+    detail::unpack(q, out);
 }
 
 }  // namespace hsgn_b200

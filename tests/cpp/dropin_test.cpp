@@ -235,6 +235,40 @@ int main() {
         CHECK(!slurp(a + "/snapshot_t0.25.csv").empty());
         CHECK(slurp(a + "/snapshot_t0.25.csv") == slurp(b + "/snapshot_t0.25.csv"));
     }
+    {  // scenario registry (scenarios.hpp:598-705): names, errors, prepare_run, exact state
+        CHECK(scenario_names().size() == 10 && scenario_names()[0] == "soliton");
+        bool threw = false;
+        try {
+            make_scenario("maelstrom");
+        } catch (const std::invalid_argument& e) {
+            threw = std::string(e.what()) == "unknown scenario 'maelstrom'";
+        }
+        CHECK(threw);
+        threw = false;
+        try {
+            make_scenario("soliton", {{"amplitud", 0.1}});
+        } catch (const std::invalid_argument& e) {
+            threw = std::string(e.what()) == "scenario 'soliton': unknown parameter 'amplitud'";
+        }
+        CHECK(threw);
+        ScenarioSpec spec = make_scenario("soliton", {{"amplitude", 0.2}});
+        CHECK(spec.lambda == 30000.0 && spec.nx_default == 200 && spec.exact_vars.size() == 2);
+        PreparedRun run = prepare_run(spec, 256, 4);
+        CHECK(run.grid.nx == 256 && run.grid.x_min == -30.0);
+        for (std::size_t k = 0; k < run.q0.h.size(); ++k) CHECK(run.q0.eta[k] == run.q0.h[k]);  // init_auxiliary
+        StateField ex(run.grid);
+        exact_state(spec, 0.0, run.grid, ex);
+        for (int i = 0; i < 256; ++i)
+            if (std::abs(run.grid.x(i)) < 29.0) CHECK(ex.h(i, 0) == run.q0.h(i, 0) && ex.u(i, 0) == run.q0.u(i, 0));
+        IntegratorConfig cfg;
+        cfg.fixed_dt = 2e-3;
+        const double m0 = total_mass(run.ctx, run.q0);
+        SolutionRecord sol = adaptive_solve(run.ctx, run.q0, 0.0, 0.2, cfg);
+        CHECK(!sol.aborted && sol.accepted == 100);
+        CHECK(std::abs(total_mass(run.ctx, sol.q) - m0) <= 1e-12 * std::abs(m0));
+        PreparedRun mms = prepare_run(make_scenario("manufactured"), 32, 32);  // forcing on the device
+        CHECK(mms.ctx.n_evals() == 0);
+    }
     std::printf("%s (%d failures)\n", failures ? "FAILED" : "PASSED", failures);
     return failures ? 1 : 0;
 }
