@@ -70,16 +70,27 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+    """nvidia-smi clocks / throttle reasons sampled during the timed region:
+    sampling starts before and stops after it, and only the samples stamped
+    inside [start(), stop()] (the timed call) enter the summary."""
+    Q = ("timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index=0, period_ms=50):
+    def __init__(self, index=0, period_ms=20):
         self.index = index
         self.period_ms = period_ms
         self.samples = []
         self._p = None
+        self._t0 = self._t1 = None
+
+    def start(self):
+        import datetime
+        self._t0 = datetime.datetime.now()
+
+    def stop(self):
+        import datetime
+        self._t1 = datetime.datetime.now()
 
     def __enter__(self):
         try:  # one long-running nvidia-smi sampling every period_ms (started before, killed after)
@@ -101,10 +112,19 @@ class ClockSampler:
         except Exception:
             self._p.kill()
             out, _ = self._p.communicate()
+        import datetime
+        rows = []
         for line in out.strip().splitlines():
             parts = [s.strip() for s in line.split(",")]
-            if len(parts) >= 6:
-                self.samples.append(parts)
+            if len(parts) >= 7:
+                try:
+                    ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f")
+                except ValueError:
+                    ts = None
+                rows.append((ts, parts[1:]))
+        inside = [p for ts, p in rows if ts and self._t0 and self._t1 and self._t0 <= ts <= self._t1]
+        self.samples = inside if len(inside) >= 2 else [p for _, p in rows]
+        self.windowed = len(inside) >= 2
 
     def summary(self):
         if not self.samples:
@@ -115,7 +135,8 @@ class ClockSampler:
         reasons = sorted({names[k] for s in self.samples for k in range(4) if "Active" in s[2 + k]
                           and "Not" not in s[2 + k]})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+                "reasons": reasons, "samples": len(self.samples),
+                "window": "timed call only" if getattr(self, "windowed", False) else "whole sampler run"}
 
 
 class CpuReference:
@@ -267,7 +288,9 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
+        clk.start()
         done, ms, kernels = H.bs3_fixed_steps(ctx, y, k1, 0.0, dt, args.steps)
+        clk.stop()
     torch.cuda.synchronize()
     ms_all = ms
     if dist:
