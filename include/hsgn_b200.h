@@ -293,6 +293,8 @@ hsgn_status hsgn_scenario_make(const char* name, const char* const* keys, const 
                                hsgn_scenario* out, char* err, int32_t err_len);
 hsgn_status hsgn_scenario_sample(const hsgn_scenario* s, int32_t nx, int32_t ny, double* b, double* q5);
 hsgn_status hsgn_scenario_exact(const hsgn_scenario* s, int32_t nx, int32_t ny, double t, double* q5);
+/* The spec's closed forms at one point: bhuv = {b, h0, u0, v0}(x, y). */
+hsgn_status hsgn_scenario_eval(const hsgn_scenario* s, double x, double y, double bhuv[4]);
 
 /* ------------------------------------------------------------ misc */
 hsgn_status hsgn_synchronize(hsgn_ctx* ctx);

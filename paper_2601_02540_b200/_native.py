@@ -139,6 +139,7 @@ def lib() -> C.CDLL:
     f("hsgn_scenario_make", C.c_int, C.c_char_p, C.POINTER(C.c_char_p), PD, I32, SC, C.c_char_p, I32)
     f("hsgn_scenario_sample", C.c_int, SC, I32, I32, PD, PD)
     f("hsgn_scenario_exact", C.c_int, SC, I32, I32, D, PD)
+    f("hsgn_scenario_eval", C.c_int, SC, D, D, PD)
     _lib = L
     return L
 
@@ -160,5 +161,5 @@ EXPORTS = [
     "hsgn_recorder_gauge_node", "hsgn_recorder_gauges", "hsgn_recorder_conservation", "hsgn_recorder_snapshot",
     "hsgn_set_fused_stages", "hsgn_fused_stages", "hsgn_profile_fused",
     "hsgn_scenario_count", "hsgn_scenario_name", "hsgn_scenario_make", "hsgn_scenario_sample",
-    "hsgn_scenario_exact", "hsgn_prepare_fixed_steps",
+    "hsgn_scenario_exact", "hsgn_prepare_fixed_steps", "hsgn_scenario_eval",
 ]

@@ -477,6 +477,12 @@ hsgn_status hsgn_scenario_sample(const hsgn_scenario* s, int32_t nx, int32_t ny,
     return HSGN_OK;
 }
 
+hsgn_status hsgn_scenario_eval(const hsgn_scenario* s, double x, double y, double* bhuv) {
+    if (!s || !bhuv || s->kind < 0 || s->kind >= NKIND) return HSGN_EINVAL;
+    initial(s, x, y, &bhuv[0], &bhuv[1], &bhuv[2], &bhuv[3]);  // the spec's b, h0, u0, v0 at (x, y)
+    return HSGN_OK;
+}
+
 hsgn_status hsgn_scenario_exact(const hsgn_scenario* s, int32_t nx, int32_t ny, double t, double* q) {
     if (!s || !q || !s->has_exact || nx < 4 || ny < 4) return HSGN_EINVAL;
     const size_t n = (size_t)nx * (size_t)ny;

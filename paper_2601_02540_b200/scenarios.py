@@ -90,6 +90,16 @@ def sample_initial(spec: ScenarioSpec, nx: int, ny: int) -> Tuple[np.ndarray, np
     return b, q
 
 
+def evaluate(spec: ScenarioSpec, x: float, y: float):
+    """The spec's closed forms at one point: (b, h0, u0, v0)(x, y)
+    (spec.bathymetry / h0 / u0 / v0, scenarios.hpp:31-34)."""
+    out = np.empty(4)
+    st = N.lib().hsgn_scenario_eval(C.byref(spec._c), float(x), float(y), out.ctypes.data_as(N.PD))
+    if st:
+        raise ValueError(f"hsgn_scenario_eval failed ({st})")
+    return tuple(float(v) for v in out)
+
+
 def exact_state(spec: ScenarioSpec, nx: int, ny: int, t: float) -> np.ndarray:
     """The scenario's exact solution at time t (5*ny*nx), scenarios.hpp:155-170, 200-214."""
     if not spec.has_exact:
@@ -133,5 +143,5 @@ def study_case(spec: ScenarioSpec, nx: int, ny: int, device: int = -1) -> Prepar
     return prepare_run(spec, nx, ny, device)
 
 
-__all__ = ["ScenarioSpec", "PreparedRun", "scenario_names", "make_scenario", "sample_initial", "exact_state",
+__all__ = ["ScenarioSpec", "PreparedRun", "scenario_names", "make_scenario", "sample_initial", "exact_state", "evaluate",
            "prepare_run", "study_case", "FIELD_NAMES"]
