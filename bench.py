@@ -84,13 +84,29 @@ class ClockSampler:
         self._p = None
         self._t0 = self._t1 = None
 
+    # cumulative microseconds each limiter held the clocks down: the delta
+    # over the timed call catches a limiter between two instantaneous samples
+    CQ = ("clocks_event_reasons_counters.sw_power_cap,clocks_event_reasons_counters.sw_thermal_slowdown,"
+          "clocks_event_reasons_counters.hw_thermal_slowdown,clocks_event_reasons_counters.hw_power_brake_slowdown")
+    CNAMES = ("sw_power_cap", "sw_thermal_slowdown", "hw_thermal_slowdown", "hw_slowdown")
+
+    def _counters(self):
+        try:
+            out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.CQ}",
+                                  "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=10).stdout
+            return [float(v) for v in out.strip().split(",")]
+        except Exception:
+            return None
+
     def start(self):
         import datetime
+        self._c0 = self._counters()
         self._t0 = datetime.datetime.now()
 
     def stop(self):
         import datetime
         self._t1 = datetime.datetime.now()
+        self._c1 = self._counters()
 
     def __enter__(self):
         try:  # one long-running nvidia-smi sampling every period_ms (started before, killed after)
@@ -132,10 +148,17 @@ class ClockSampler:
         sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
         mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for s in self.samples for k in range(4) if "Active" in s[2 + k]
-                          and "Not" not in s[2 + k]})
+        reasons = {names[k] for s in self.samples for k in range(4) if "Active" in s[2 + k] and "Not" not in s[2 + k]}
+        held = {}
+        c0, c1 = getattr(self, "_c0", None), getattr(self, "_c1", None)
+        if c0 and c1 and len(c0) == len(c1) == 4:
+            for k, nm in enumerate(self.CNAMES):
+                if c1[k] > c0[k]:
+                    reasons.add(nm)
+                    held[nm + "_ms"] = (c1[k] - c0[k]) / 1e3
+        reasons = sorted(reasons)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples),
+                "reasons": reasons, "limiter_ms": held, "samples": len(self.samples),
                 "window": "timed call only" if getattr(self, "windowed", False) else "whole sampler run"}
 
 
