@@ -5,23 +5,38 @@ Metric (BASELINE.json): grid-point RK-stage updates per second on an 8192^2
 fp64 grid (config 4: periodic [-1,1]^2, manufactured bathymetry and state at
 t = 0.3, lambda = 500, fixed dt = 0.25 dx / 20), plus achieved HBM GB/s.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--n 8192]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--bc periodic|reflecting] [--scaling weak|strong] [--config5]
+                    [--n NX] [--rows R] [--sustained S]
 
 * ``value``   : point-stage updates/s, device time (CUDA events on the
-                library stream) of K graph-captured fused steps, inputs
-                resident in HBM; every state is 2.7 GB (> 126 MB L2), so no
-                L2 flush is needed between steps.
+                library stream, max over ranks) of one hsgn_bs3_fixed_steps
+                call of K graph-captured fused steps, in place on resident
+                states; every state is >= 2.7 GB (> 126 MB L2), so no L2
+                flush is needed between steps.
 * ``e2e``     : the same metric through the public API with HOST buffers:
-                one ``adaptive_solve`` call (fixed dt, K steps) from a pinned
-                host state to a host result, H2D + D2H inside the timed region.
-* ``roofline``: the dominant kernel of the steady-state step (S2 or the
-                fused S3+S1 kernel S31, DESIGN.md sections 2b, 7), algorithmic
-                bytes per launch (168 / 128 B per node) / its mean launch time.
-* ``cpu_baseline``: the reference CPU path (oracle/_ref, or the C oracle port)
-                on this host's cores on a bounded sample.
-Multi-GPU (torchrun): weak scaling, every rank owns an 8192-row slab of a
-(8192 x 8192*N) periodic grid; halo rows via NCCL.  ``--impl reference``
-runs the reference CPU implementation only on rank 0.
+                upload of the pinned host state, one ``adaptive_solve`` call
+                (fixed dt, K steps, incl. its initial RHS) and the download of
+                the result, all inside the wall-clock window (device buffers
+                allocated before it).
+* ``roofline``: the dominant kernel S12 (stages 1 + 2)
+                on SURVEY section 8(d)'s roofline: 128 B per point-stage x the
+                2 point-stages S12 updates per node, over its mean launch time
+                measured by CUDA event nodes inside the timed graphs; with its
+                own-byte HBM fraction and its FP64-pipe fraction beside it.
+* ``sustained``: the same measurement over S steps (default 300, ~1.3 s):
+                the power-capped long-run rate.
+* ``cpu_baseline``: the reference CPU path (oracle/_ref, the unmodified
+                reference compiled in place; else the C oracle port) on this
+                host's cores, on the same workload (all threads, median of
+                reps) plus a 1-thread line on a 2048^2 slice.
+Multi-GPU: ``--gpus N`` outside torchrun launches N ranks itself
+(torch.distributed.run; it refuses when fewer than N GPUs are visible); each
+rank owns a y-slab, halos and the step agreement go over NCCL inside the
+captured graphs.  Weak scaling (default): every rank owns an NX x R slab of
+an NX x (R N) grid (default 8192 x 8192, the config-4 block; --config5:
+16384 x 4096); strong: a fixed NX x NY grid (default 16384^2 at N > 1).
+``--impl reference`` runs the reference CPU implementation only on rank 0.
 """
 from __future__ import annotations
 
@@ -33,31 +48,19 @@ import subprocess
 import sys
 import time
 
-import numpy as np
-
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-BYTES_PER_NODE = {"S1": 128, "S2": 168, "S3": 88, "S31": 128, "STEP": 168, "S12": 128}
-BYTES_PER_POINT_STAGE = 128  # unfused step: 384 B per node / 3 stages
+BYTES_PER_POINT_STAGE = 128  # unfused compulsory traffic per grid-point RK stage
+OWN_BYTES_PER_NODE = {"S12": 128, "S3": 88}  # y, k1, b -> ynew; ynew, b -> k4
+POINT_STAGES_PER_NODE = {"S12": 2, "S3": 1}
 # FP64 instructions (DADD + DMUL + DFMA) per node of each kernel, from the ncu
-# SASS mixes in profiles/ (r1_sass_mix_stage_kernels.txt, r1f_sass_mix_s31.txt,
-# r1k_sass_mix_s12.txt, r1k_sass_mix_s3.txt): the compute roofline of the FP64-issue-bound kernels
-FP64_PER_NODE = {"S1": 199.5, "S2": 228.8, "S3": 189.1, "S31": 397.3, "S12": 437.5}
+# SASS mixes in profiles/ (the compute roofline of the FP64-issue-bound kernels)
+FP64_PER_NODE = {"S12": 437.5, "S3": 189.1}
+FP64_SOURCE = "profiles/r1k_sass_mix_s12.txt, profiles/r1k_sass_mix_s3.txt"
 FP64_LANES_PER_SM, N_SM = 64, 148
-
-
-def step_bytes_per_node(mode: int, chunk: int) -> float:
-    """Algorithmic HBM bytes per node per step of the fixed-step pipeline:
-    mode 0 S1 + S2 + S3 = 384; mode 1 chunks of n steps S1 + n S2 +
-    (n-1) S31 + S3 = 296 n + 88; mode 2 one whole-step kernel = 168;
-    mode 3 S12 + S3 = 128 + 88 = 216."""
-    if mode == 0:
-        return 384.0
-    if mode == 1:
-        return (296.0 * chunk + 88.0) / chunk
-    return 168.0 if mode == 2 else 216.0
 METRIC = "grid-point RK-stage updates/sec on 8192² fp64 grid; achieved HBM GB/s"
+UNIT = "point-stage updates/s"
 
 
 def peaks():
@@ -65,8 +68,19 @@ def peaks():
     if os.path.exists(p):
         with open(p) as fh:
             d = json.load(fh)
-        return float(d.get("hbm_gbs", 6650.0)), "measured"
-    return 6650.0, "fallback"
+        return float(d.get("hbm_gbs", 6650.0)), "MEASURED_PEAKS.json hbm_gbs (burst copy)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(kernel: str):
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full
+    capture (profiles/traffic.json), with its source."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(p):
+        return None, None
+    with open(p) as fh:
+        d = json.load(fh)
+    return d.get(kernel), d.get("_source")
 
 
 class ClockSampler:
@@ -75,7 +89,12 @@ class ClockSampler:
     inside [start(), stop()] (the timed call) enter the summary."""
     Q = ("timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+         "clocks_event_reasons.sw_power_cap,power.draw")
+    # cumulative microseconds each limiter held the clocks down: the delta
+    # over the timed call catches a limiter between two instantaneous samples
+    CQ = ("clocks_event_reasons_counters.sw_power_cap,clocks_event_reasons_counters.sw_thermal_slowdown,"
+          "clocks_event_reasons_counters.hw_thermal_slowdown,clocks_event_reasons_counters.hw_power_brake_slowdown")
+    CNAMES = ("sw_power_cap", "sw_thermal_slowdown", "hw_thermal_slowdown", "hw_slowdown")
 
     def __init__(self, index=0, period_ms=20):
         self.index = index
@@ -83,12 +102,7 @@ class ClockSampler:
         self.samples = []
         self._p = None
         self._t0 = self._t1 = None
-
-    # cumulative microseconds each limiter held the clocks down: the delta
-    # over the timed call catches a limiter between two instantaneous samples
-    CQ = ("clocks_event_reasons_counters.sw_power_cap,clocks_event_reasons_counters.sw_thermal_slowdown,"
-          "clocks_event_reasons_counters.hw_thermal_slowdown,clocks_event_reasons_counters.hw_power_brake_slowdown")
-    CNAMES = ("sw_power_cap", "sw_thermal_slowdown", "hw_thermal_slowdown", "hw_slowdown")
+        self._c0 = self._c1 = None
 
     def _counters(self):
         try:
@@ -132,7 +146,7 @@ class ClockSampler:
         rows = []
         for line in out.strip().splitlines():
             parts = [s.strip() for s in line.split(",")]
-            if len(parts) >= 7:
+            if len(parts) >= 8:
                 try:
                     ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f")
                 except ValueError:
@@ -145,21 +159,56 @@ class ClockSampler:
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+
+        def num(v):
+            try:
+                return float(v)
+            except ValueError:
+                return None
+        sm = [x for x in (num(s[0]) for s in self.samples) if x is not None]
+        mx = [x for x in (num(s[1]) for s in self.samples) if x is not None]
+        pw = [x for x in (num(s[6]) for s in self.samples) if x is not None]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = {names[k] for s in self.samples for k in range(4) if "Active" in s[2 + k] and "Not" not in s[2 + k]}
         held = {}
-        c0, c1 = getattr(self, "_c0", None), getattr(self, "_c1", None)
+        c0, c1 = self._c0, self._c1
         if c0 and c1 and len(c0) == len(c1) == 4:
             for k, nm in enumerate(self.CNAMES):
                 if c1[k] > c0[k]:
                     reasons.add(nm)
                     held[nm + "_ms"] = (c1[k] - c0[k]) / 1e3
-        reasons = sorted(reasons)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "limiter_ms": held, "samples": len(self.samples),
+                "reasons": sorted(reasons), "limiter_ms": held, "power_w_median": statistics.median(pw) if pw else None,
+                "samples": len(self.samples),
                 "window": "timed call only" if getattr(self, "windowed", False) else "whole sampler run"}
+
+
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def keep_heap():
+    """glibc: serve the reference's field allocations from the heap and never
+    trim it, so a solve reuses the pages the previous one touched instead of
+    page-faulting its ~44 GB workspace (8192^2) anew.  The reference
+    allocates its workspace per adaptive_solve call; in its own CLI that is
+    once per run, amortised over thousands of steps -- this keeps a short
+    timed solve representative of that.  (Allocator tuning of this process
+    only; the reference code is unchanged.)"""
+    import ctypes
+    try:
+        libc = ctypes.CDLL("libc.so.6")
+        libc.mallopt(-4, 0)   # M_MMAP_MAX: no mmap'ed chunks
+        libc.mallopt(-1, -1)  # M_TRIM_THRESHOLD: never trim the heap top
+    except Exception:
+        pass
 
 
 class CpuReference:
@@ -167,80 +216,149 @@ class CpuReference:
     oracle/_ref (the unmodified reference headers compiled in place; OpenMP)
     when it was built, else the C oracle port.  A "step" is one fixed-step
     BS3 step (time_integration.hpp:262-345: 3 RHS + stage axpys + min-h) of
-    an n^2 sample of the benchmark workload (same closed-form input)."""
+    the same workload (same closed-form input)."""
 
-    def __init__(self, n: int):
+    def __init__(self, bc: str, nx: int, ny: int, threads: int = 0):
+        keep_heap()
         sys.path.insert(0, os.path.join(ROOT, "tests"))
-        from oracle_lib import PD, Oracle, Phys, default_cfg, make_grid as omake, ref_available
-        from paper_2601_02540_b200.workloads import mms_fields
+        from oracle_lib import Oracle, Phys, default_cfg, make_grid as omake, ref_available
+        from paper_2601_02540_b200.workloads import bench_case
         self.kind = "reference" if ref_available() else "port"
         self.orc = Oracle("ref" if self.kind == "reference" else "orc")
-        self.cores = os.cpu_count() or 1
+        self.cores = threads or (os.cpu_count() or 1)
         self.orc.set_threads(self.cores)
-        self.n = n
-        g, self.q, self.b = mms_fields(n, n, 0.3)
-        self.og = omake(n, n)
-        self.dt = 0.25 * g.dx / 20.0
-        self.ph = Phys(9.81, 500.0, 1e-12)
+        self.nx, self.ny, self.bc = nx, ny, bc
+        g, self.q, self.b, lam, self.dt, aux = bench_case(bc, nx, ny)
+        kx = ky = 1 if bc == "reflecting" else 0
+        self.og = omake(nx, ny, g.x_min, g.x_max, g.y_min, g.y_max, kx, ky)
+        if aux:  # w, eta = init_auxiliary (model.hpp:93-105), the reference's own
+            self.q = self.orc.init_auxiliary(self.og, self.b, self.q)
+        self.ph = Phys(9.81, lam, 1e-12)
         self.cfg = default_cfg
-        self._pd = PD
 
     def steps(self, k: int) -> float:
         """Wall seconds of k fixed steps, minus the initial tendency the
-        solve evaluates first (timed separately as one RHS)."""
+        solve evaluates first (its share of the 3k + 1 evaluations)."""
         t0 = time.perf_counter()
         _, rec = self.orc.solve(self.og, self.ph, self.b, self.q, 0.0, k * self.dt, self.cfg(fixed_dt=self.dt))
         el = time.perf_counter() - t0
         assert rec.accepted == k and not rec.aborted
-        return el * (3 * k) / (3 * k + 1)  # drop the k1 = f(y0) evaluation's share
+        return el * (3 * k) / (3 * k + 1)
 
-    def describe(self, k, seconds):
-        return {"value": 3 * k * self.n * self.n / seconds, "unit": "point-stage updates/s", "cores": self.cores,
-                "kind": self.kind,
-                "sample": f"{self.n}x{self.n} slice of the config-4 workload (periodic, manufactured state "
-                          f"t=0.3, lambda=500), {k} fixed BS3 steps via the reference adaptive_solve(fixed_dt), "
-                          f"{seconds:.2f} s wall on {self.cores} threads"}
+    def rate(self, k, seconds):
+        return 3 * k * self.nx * self.ny / seconds
 
 
-def cpu_baseline(n_sample: int = 2048, steps: int = 12):
-    ref = CpuReference(n_sample)
-    ref.steps(1)  # warm-up: page-in, OpenMP pool
-    return ref.describe(steps, ref.steps(steps))
+def cpu_baseline(bc: str, nx: int, ny: int, reps: int = 3, steps: int = 2):
+    """cmd_bench-style (cli.hpp:248-268) median of reps on the full workload
+    with every host thread, plus a 1-thread line on a 2048^2 slice."""
+    ref = CpuReference(bc, nx, ny)
+    ref.steps(1)  # warm-up: page-in, OpenMP pool, first touch of the workspace
+    secs = [ref.steps(steps) for _ in range(reps)]
+    med = statistics.median(secs)
+    n1 = min(2048, nx)
+    one = CpuReference(bc, n1, n1, threads=1)
+    t1 = one.steps(1)
+    return {"value": ref.rate(steps, med), "unit": UNIT, "cores": ref.cores, "kind": ref.kind, "cpu": cpu_model(),
+            "sample": f"the full {nx}x{ny} {bc} workload, {steps} fixed BS3 steps per rep via the reference "
+                      f"adaptive_solve(fixed_dt), median of {reps} reps ({', '.join(f'{s:.2f}' for s in secs)} s) "
+                      f"on {ref.cores} OpenMP threads",
+            "one_thread": {"value": one.rate(1, t1), "cores": 1,
+                           "sample": f"{one.nx}x{one.ny} slice, 1 fixed step, {t1:.2f} s"}}
 
 
-def workload_config(n: int, world: int) -> dict:
-    """The workload both arms report (BASELINE config 4; weak scaling stacks
-    8192-row slabs)."""
-    nyg = n * world
-    return {"workload": f"config 4: {n}x{nyg} periodic, manufactured bathymetry + state "
-                        f"(t=0.3), lambda=500, fixed-step BS3 dt=0.25dx/20",
-            "grid": f"{n}x{nyg}", "points": n * nyg, "parallelism": f"slab{world}"}
+def shapes(args, world: int):
+    """(nx, global ny, scaling) of the run."""
+    if args.scaling == "strong":
+        nx = args.n or (16384 if args.config5 or world > 1 else 8192)
+        return nx, args.ny or nx, "strong"
+    nx = args.n or (16384 if args.config5 else 8192)
+    rows = args.rows or (4096 if args.config5 else nx)
+    return nx, rows * world, "weak"
+
+
+def workload_config(args, nx: int, ny: int, world: int, scaling: str) -> dict:
+    bc = args.bc
+    if world > 1 or args.config5:
+        what = f"config 5 ({scaling} scaling)"
+    elif bc == "periodic":
+        what = "config 4" if nx == ny == 8192 else "config-4 input"
+    else:
+        what = "config-3/5 reflecting walls"
+    if bc == "periodic":
+        desc = (f"{what}: {nx}x{ny} periodic, manufactured bathymetry + state (t=0.3) on "
+                f"[-1,1]x[-1,{-1 + 2 * ny / nx:g}], lambda=500, fixed-step BS3 dt=0.25dx/20")
+    else:
+        desc = (f"{what}: {nx}x{ny} reflecting walls, gaussian_obstacle(bounded) on [-5,35]x[-10,10], lambda=500, "
+                f"fixed-step BS3 dt=0.25min(dx,dy)/20")
+    return {"workload": desc, "bc": bc, "grid": f"{nx}x{ny}", "points": nx * ny, "scaling": scaling,
+            "parallelism": f"slab{world}" if world > 1 else "1 GPU, whole grid"}
 
 
 def run_reference(args):
     """--impl reference: the reference's own CPU implementation, timed per
-    step on this host's cores (rank 0 only under torchrun)."""
+    step on this host's cores (rank 0 only under torchrun), on the same
+    workload as the device arm (the full grid up to the 8192^2 config-4 size,
+    which needs ~44 GB of reference workspace; beyond it one rank's share)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    ref = CpuReference(args.ref_n)
+    world = max(1, args.gpus)
+    nx, ny, scaling = shapes(args, world)
+    ny_ref = ny if nx * ny <= 8192 * 8192 else max(4, ny // world)
+    ref = CpuReference(args.bc, nx, ny_ref)
     ref.steps(max(1, args.warmup))  # warm-up steps (page-in, OpenMP pool, workspace first touch)
     total = ref.steps(args.steps)   # K steps in one solve, as the reference integrates
-    cb = ref.describe(args.steps, total)
-    v = cb["value"]
-    line = {"metric": METRIC, "value": v, "unit": "point-stage updates/s", "n_gpus": args.gpus,
+    v = ref.rate(args.steps, total)
+    cb = {"value": v, "unit": UNIT, "cores": ref.cores, "kind": ref.kind, "cpu": cpu_model(),
+          "sample": f"{nx}x{ny_ref} of the {args.bc} workload, {args.steps} fixed BS3 steps in one reference "
+                    f"adaptive_solve(fixed_dt) ({total:.2f} s) after {max(1, args.warmup)} warm-up steps, "
+                    f"{ref.cores} OpenMP threads"}
+    cfg = workload_config(args, nx, ny, world, scaling)
+    cfg.update(parallelism="cpu-openmp", reference_grid=f"{nx}x{ny_ref}", same_config=(ny_ref == ny))
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "impl": "reference",
-            # the same workload as the device arm; each step runs on the bounded
-            # sample cpu_baseline.sample states (host cores, OpenMP)
-            "config": dict(workload_config(args.n, args.gpus), parallelism="cpu-openmp",
-                           sample=f"{args.ref_n}x{args.ref_n} slice per step"),
-            "cpu_baseline": cb,
-            "e2e": {"value": v, "unit": "point-stage updates/s", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
-    print(json.dumps(line))
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference", "config": cfg, "cpu_baseline": cb,
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
     return 0
+
+
+def visible_gpus() -> int:
+    try:
+        out = subprocess.run(["nvidia-smi", "-L"], capture_output=True, text=True, timeout=30).stdout
+        return sum(1 for line in out.splitlines() if line.startswith("GPU "))
+    except Exception:
+        return 0
+
+
+def refuse(args, n_dev: int) -> int:
+    """Fewer GPUs than --gpus asks for: say so and exit 2 (never time fewer
+    GPUs than the line reports)."""
+    sys.stderr.write(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, this node has {n_dev}; "
+                     f"refusing to time fewer GPUs than requested\n")
+    if int(os.environ.get("RANK", "0")) == 0:
+        print(json.dumps({"metric": METRIC, "n_gpus": args.gpus,
+                          "error": f"--gpus {args.gpus} requested, {n_dev} GPU(s) visible"}), flush=True)
+    return 2
+
+
+def self_launch(args) -> int:
+    """--gpus N > 1 outside torchrun: start N ranks (one per GPU) with
+    torch.distributed.run on this node; rank 0 prints the line."""
+    n_dev = visible_gpus()
+    if n_dev < args.gpus:
+        return refuse(args, n_dev)
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # the communicator's rank count is in the log
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
 
 
 def main():
@@ -249,25 +367,35 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=8192)
-    ap.add_argument("--ref-n", type=int, default=2048)
-    ap.add_argument("--ref-steps", type=int, default=12)
+    ap.add_argument("--bc", default="periodic", choices=["periodic", "reflecting"])
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--config5", action="store_true", help="SURVEY config-5 shapes (16384 wide)")
+    ap.add_argument("--n", type=int, default=0, help="nx (default 8192; 16384 for --config5 / strong N>1)")
+    ap.add_argument("--rows", type=int, default=0, help="weak scaling: rows per rank (default nx; 4096 --config5)")
+    ap.add_argument("--ny", type=int, default=0, help="strong scaling: global rows (default nx)")
+    ap.add_argument("--sustained", type=int, default=300, help="steps of the sustained-rate run (0: skip)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--rows-per-block", type=int, default=0)
-    ap.add_argument("--fusion", type=int, default=-1, choices=[-1, 0, 1, 2, 3],
-                    help="fixed-step kernel structure (0 per stage, 1 S31, 2 whole step, 3 S12 + S3; "
-                         "-1 library default)")
+    ap.add_argument("--fusion", type=int, default=-1, choices=[-1, 0, 3],
+                    help="fixed-step kernel structure (0 per stage, 3 S12 + S3; -1 library default)")
     ap.add_argument("--slab-ring", action="store_true",
                     help="N=1 only: run the P-rank slab code path as a 1-rank NCCL ring (halos to itself)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(args)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        sys.stderr.write(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}\n")
+        return 2
     import torch
+    if torch.cuda.device_count() < max(world, local + 1):
+        return refuse(args, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dist = None
     if world > 1 or args.slab_ring:
@@ -281,90 +409,99 @@ def main():
 
     import paper_2601_02540_b200 as H
     from paper_2601_02540_b200 import slab as S
-    from paper_2601_02540_b200.workloads import mms_fields
+    from paper_2601_02540_b200.workloads import bench_case
 
-    n = args.n
-    nyg = n * world
+    nx, nyg, scaling = shapes(args, world)
     slabbed = world > 1 or args.slab_ring
-    g, q, b = mms_fields(n, nyg, 0.3) if not slabbed else S.slab_fields(n, nyg, 0.3, rank, world)
-    dt = 0.25 * (2.0 / n) / 20.0
-    phys = H.PhysSetup(9.81, 500.0, 1e-12, b.reshape(-1, n))
-    if not slabbed:
-        ctx = H.make_rhs_context(g, phys, device=local)
-    else:
-        ctx = S.make_slab_context(g, phys, rank, world, local, dist)
+    j0, j1 = S.partition(nyg, world)[rank]
+    g, q, b, lam, dt, needs_aux = bench_case(args.bc, nx, nyg, rows=(j0, j1))
+    phys = H.PhysSetup(9.81, lam, 1e-12, b.reshape(-1, nx))
+    ctx = (S.make_slab_context(g, phys, rank, world, local, dist) if slabbed else
+           H.make_rhs_context(g, phys, device=local))
     if args.rows_per_block:
         ctx.set_rows_per_block(args.rows_per_block)
     if args.fusion >= 0:
         ctx.fused_stages = args.fusion
-    mode = ctx.fused_stages if not slabbed else (3 if ctx.fused_stages == 3 else 0)  # slabs: S12 + S3 or per stage
     y = ctx.state(q)
+    if needs_aux:  # w, eta of the reflecting workload (model.hpp:93-105, on the device)
+        H.init_auxiliary(ctx, y)
+        q = y.download().flat().copy()
     k1 = ctx.state()
     H.rhs(ctx, 0.0, y, k1)
-    points = n * ctx.ny_local
+    points = nx * ctx.ny_local
 
-    # warm-up; the CUDA graphs of the timed K-step call are built here too
-    # (capture + instantiation is one-time host work, not a step)
-    H.bs3_fixed_steps(ctx, y, k1, 0.0, dt, args.warmup)
-    H.prepare_fixed_steps(ctx, dt, args.steps)
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
-        clk.start()
-        done, ms, kernels = H.bs3_fixed_steps(ctx, y, k1, 0.0, dt, args.steps)
-        clk.stop()
-    torch.cuda.synchronize()
-    ms_all = ms
-    if dist:
-        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+    def max_over_ranks(v):
+        if not dist:
+            return v
+        t = torch.tensor([v], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_all = float(t.item())
+        return float(t.item())
+
+    def timed_steps(k, kernel_timing):
+        """One hsgn_bs3_fixed_steps call of k steps (graphs built before the
+        window); returns (done, max-over-ranks device ms, kernels, clocks)."""
+        H.set_kernel_timing(ctx, kernel_timing)
+        H.prepare_fixed_steps(ctx, y, k1, dt, k)
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        with ClockSampler(local) as clk:
+            clk.start()
+            done, ms, kernels = H.bs3_fixed_steps(ctx, y, k1, 0.0, dt, k)
+            clk.stop()
+        torch.cuda.synchronize()
+        return done, max_over_ranks(ms), kernels, clk.summary()
+
+    # warm-up (page-in, module load, first graph launches)
+    H.set_kernel_timing(ctx, True)
+    H.bs3_fixed_steps(ctx, y, k1, 0.0, dt, args.warmup)
+    # the timed region: K steps; CUDA event nodes around every kernel of the
+    # captured graphs give the per-kernel durations of this very call
+    done, ms_all, kernels, clocks = timed_steps(args.steps, True)
+    s12_ms, s3_ms, kt_steps = H.kernel_times(ctx)
     value = 3 * points * world * args.steps / (ms_all * 1e-3)
 
-    # per-kernel times for the roofline (same stream, CUDA events)
-    ms3 = (H.api.N.D * 3)()
-    H.api._check(ctx, H.api.N.lib().hsgn_profile_stages(ctx._h, y._h, k1._h, dt, 3, ms3), "profile")
-    ms3 = list(ms3)
-    names = ["S1", "S2", "S3"]
-    if mode:  # steady-state step: S2 + S31 (mode 1), STEP (mode 2), S12 + S3 (mode 3)
-        mf = H.api.N.D(0.0)
-        H.api._check(ctx, H.api.N.lib().hsgn_profile_fused(ctx._h, y._h, k1._h, dt, 3, H.api.C.byref(mf)),
-                     "profile_fused")
-        ms3.append(mf.value)
-        names.append({1: "S31", 2: "STEP", 3: "S12"}[mode])
-    cand = {0: [0, 1, 2], 1: [1, 3], 2: [3], 3: [2, 3]}[mode]
-    dom = max(cand, key=lambda k: ms3[k])
-    peak, peak_kind = peaks()
-    achieved = BYTES_PER_NODE[names[dom]] * points / (ms3[dom] * 1e-3) / 1e9
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tpath):
-        with open(tpath) as fh:
-            traffic = json.load(fh).get(names[dom])
-    fp64 = None
-    if names[dom] in FP64_PER_NODE:
-        sm_mhz = clk.summary().get("sm_mhz") or 1965.0
-        got = FP64_PER_NODE[names[dom]] * points / (ms3[dom] * 1e-3) / 1e9
-        top = FP64_LANES_PER_SM * N_SM * sm_mhz * 1e-3
-        fp64 = {"unit": "G FP64 thread-instr/s", "instr_per_node": FP64_PER_NODE[names[dom]], "achieved": got,
-                "peak": top, "frac": got / top, "peak_basis": f"{FP64_LANES_PER_SM} lanes x {N_SM} SMs x sm_mhz"}
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "fp64": fp64,
-                "traffic": traffic,
-                "kernel": {"S31": "sgn_s31_kernel", "STEP": "sgn_step_kernel", "S12": "sgn_s12_kernel"}.get(
-                    names[dom], f"sgn_stage_kernel<{names[dom]}>"),
-                "fixed_step_kernels": ["per stage", "S2 + S31", "whole step", "S12 + S3"][mode],
-                "bytes_per_node": BYTES_PER_NODE[names[dom]], "peak_source": peak_kind,
-                "stage_ms": {names[k]: ms3[k] for k in range(len(names))},
-                "step_bytes_per_node": step_bytes_per_node(mode, min(64, args.steps)),
-                # updates/s x 128 B (the unfused compulsory traffic per
-                # point-stage) against the HBM peak; fusion removes traffic, so this
-                # equivalent-bandwidth fraction exceeds the fused kernels' own
-                "equiv_unfused": {"bytes_per_point_stage": BYTES_PER_POINT_STAGE,
-                                  "achieved": value * BYTES_PER_POINT_STAGE / 1e9,
-                                  "frac": value * BYTES_PER_POINT_STAGE / 1e9 / peak},
-                "step_gbs": step_bytes_per_node(mode, min(64, args.steps)) * points / (ms / args.steps * 1e-3) / 1e9}
+    # roofline of the dominant kernel (S12): SURVEY 8(d) and own-byte views
+    peak, peak_src = peaks()
+    sm_mhz = clocks.get("sm_mhz") or 1965.0
+    fp64_peak = FP64_LANES_PER_SM * N_SM * sm_mhz * 1e-3  # G thread-instr/s at the sampled clock
+    roofline = None
+    if kt_steps and s12_ms > 0:
+        kern = {}
+        for name, t_ms in (("S12", s12_ms), ("S3", s3_ms)):
+            sec = t_ms * 1e-3
+            eq = BYTES_PER_POINT_STAGE * POINT_STAGES_PER_NODE[name] * points / sec / 1e9
+            own = OWN_BYTES_PER_NODE[name] * points / sec / 1e9
+            f64 = FP64_PER_NODE[name] * points / sec / 1e9
+            kern[name] = {"ms": t_ms, "equiv_gbs": eq, "equiv_frac": eq / peak,
+                          "own_bytes_per_node": OWN_BYTES_PER_NODE[name], "own_gbs": own, "own_frac": own / peak,
+                          "fp64_instr_per_node": FP64_PER_NODE[name], "fp64_g_per_s": f64,
+                          "fp64_frac": f64 / fp64_peak}
+        traffic, tsrc = ncu_traffic("S12")
+        dom = kern["S12"]
+        roofline = {
+            "bound": "hbm", "achieved": dom["equiv_gbs"], "peak": peak, "unit": "GB/s", "frac": dom["equiv_frac"],
+            "traffic": traffic, "traffic_source": tsrc,
+            "kernel": "sgn_s12_kernel (stages 1+2 of a BS3 step)",
+            "definition": "SURVEY 8(d): 128 B per grid-point RK stage x 2 stages per node per S12 launch / mean "
+                          "S12 launch time (CUDA event nodes inside the timed graphs)",
+            "limiter": "FP64 dependency latency (own-byte HBM and FP64-pipe fractions below)",
+            "own_bytes_frac": dom["own_frac"], "fp64_frac": dom["fp64_frac"],
+            "fp64_peak_g_per_s": fp64_peak, "fp64_source": FP64_SOURCE, "peak_source": peak_src,
+            "kernels": kern, "kernel_ms_steps_timed": kt_steps, "step_ms": ms_all / args.steps,
+            "step_own_gbs": (OWN_BYTES_PER_NODE["S12"] + OWN_BYTES_PER_NODE["S3"]) * points
+            / (ms_all / args.steps * 1e-3) / 1e9}
+
+    # the same call without event nodes (the launch stream as shipped)
+    done_b, ms_b, _, clocks_b = timed_steps(args.steps, False)
+    plain = {"value": 3 * points * world * args.steps / (ms_b * 1e-3), "ms_per_step": ms_b / args.steps,
+             "clocks": clocks_b}
+
+    sustained = None
+    if args.sustained > 0:
+        done_s, ms_s, _, clocks_s = timed_steps(args.sustained, False)
+        sustained = {"steps": args.sustained, "value": 3 * points * world * args.sustained / (ms_s * 1e-3),
+                     "ms_per_step": ms_s / args.sustained, "clocks": clocks_s}
 
     # end-to-end through the public API with host buffers (pinned); at N > 1
     # every rank integrates its slab (halos and the step agreement over NCCL)
@@ -374,27 +511,25 @@ def main():
         host = torch.empty(q.size, dtype=torch.float64).pin_memory()
         host.numpy()[:] = q
         res_host = torch.empty(q.size, dtype=torch.float64).pin_memory()
-        st_in = H.StateField((ny_l, n), host.numpy())
+        st_in = H.StateField((ny_l, nx), host.numpy())
+        st_out = H.StateField((ny_l, nx), res_host.numpy())
         cfg = H.IntegratorConfig(fixed_dt=dt)
-        out_state = ctx.state()
-        # warm: the same call, so the timed one reuses its CUDA graphs
-        H.adaptive_solve(ctx, st_in, 0.0, args.steps * dt, cfg, out=out_state)
+        dq0, out_state = ctx.state(), ctx.state()  # device buffers: allocated outside the window
+        dq0.upload(st_in)
+        H.adaptive_solve(ctx, dq0, 0.0, args.steps * dt, cfg, out=out_state)  # warm: builds its graphs
         if dist:
             dist.barrier()
+        torch.cuda.synchronize()
         t0 = time.perf_counter()
-        dq0 = ctx.state(st_in)                        # H2D of the host state
+        dq0.upload(st_in)                                                  # H2D of the host state
         rec = H.adaptive_solve(ctx, dq0, 0.0, args.steps * dt, cfg, out=out_state)
-        out_state.download(H.StateField((ny_l, n), res_host.numpy()))  # D2H of the result
-        el = time.perf_counter() - t0
-        if dist:
-            t = torch.tensor([el], device="cuda", dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            el = float(t.item())
+        out_state.download(st_out)                                         # D2H of the result
+        el = max_over_ranks(time.perf_counter() - t0)
         nbytes = 5 * points * 8 * world
-        e2e = {"value": 3 * points * world * rec.accepted / el, "unit": "point-stage updates/s",
+        e2e = {"value": 3 * points * world * rec.accepted / el, "unit": UNIT,
                "h2d_bytes_per_step": nbytes / args.steps, "d2h_bytes_per_step": nbytes / args.steps,
-               "api": "adaptive_solve(host q0 -> host q, fixed_dt, K steps) incl. initial RHS"
-                      + (" per slab rank, max over ranks" if world > 1 else ""),
+               "api": "upload(pinned host q0) + adaptive_solve(fixed_dt, K steps, incl. initial RHS) + "
+                      "download(q) -> pinned host" + (" per slab rank, max over ranks" if world > 1 else ""),
                "wall_s": el}
         dq0.free()
         out_state.free()
@@ -402,23 +537,25 @@ def main():
     cb = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cb = cpu_baseline(args.ref_n, args.ref_steps)
+            cb = cpu_baseline(args.bc, nx, nyg)
         except Exception as ex:  # the baseline never gates the GPU number
             cb = {"value": None, "error": str(ex)}
 
     if rank == 0:
-        line = {"metric": METRIC, "value": value, "unit": "point-stage updates/s", "n_gpus": world,
+        cfg = workload_config(args, nx, nyg, world, scaling)
+        cfg.update(l2="inputs > L2 (>= 2.7 GB per state, 126 MB L2); no flush needed",
+                   rows_per_block=args.rows_per_block or "auto",
+                   fixed_step_kernels="S12 + S3" if ctx.fused_stages == 3 else "one kernel per stage")
+        if slabbed and world == 1:
+            cfg["parallelism"] = "slab1 as a 1-rank NCCL ring (the P-rank code path)"
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_all / args.steps,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic",
-                "config": dict(workload_config(n, world),
-                               l2="inputs > L2 (2.7 GB per state); no flush needed",
-                               rows_per_block=args.rows_per_block or "auto",
-                               **({"parallelism": "slab1 as a 1-rank NCCL ring (the P-rank code path)"}
-                                  if slabbed and world == 1 else {})),
-                "hbm_gbs": roofline["step_gbs"], "roofline": roofline, "cpu_baseline": cb, "e2e": e2e,
-                "gpu_launches": kernels, "clocks": clk.summary(), "steps_done": done}
-        print(json.dumps(line))
+                "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic", "config": cfg,
+                "hbm_gbs": roofline["step_own_gbs"] if roofline else None,
+                "roofline": roofline, "cpu_baseline": cb, "e2e": e2e, "gpu_launches": kernels,
+                "clocks": clocks, "without_event_nodes": plain, "sustained": sustained, "steps_done": done}
+        print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()
         dist.destroy_process_group()

@@ -118,18 +118,10 @@ hsgn_status hsgn_set_rows_per_block(hsgn_ctx* ctx, int32_t rows);
 hsgn_status hsgn_set_stencil_kind(hsgn_ctx* ctx, int32_t kind);
 int32_t hsgn_stencil_kind(const hsgn_ctx* ctx);
 
-/* Raw-input staging: 1 = TMA bulk copies into a shared-memory ring two rows
- * ahead (needs nx even), 0 = register prefetch one row ahead (default: it
- * measured faster in round 1).  Both are bit-identical;
- * the switch exists for tests and measurements. */
-hsgn_status hsgn_set_tma(hsgn_ctx* ctx, int32_t on);
-int32_t hsgn_tma_enabled(const hsgn_ctx* ctx);
-
-/* Kernel structure of the fixed-step graphs of a whole-grid context (all
+/* Kernel structure of the fixed steps and adaptive attempts (both
  * bit-identical): 0 = one kernel per stage,
- * 1 = stage 3 of step n fused with stage 1 of step n+1 (S31), 2 = one
- * kernel per whole step, 3 (default) = stages 1+2 fused (S12), then stage 3.
- * Slab contexts always run one kernel per stage. */
+ * 3 (default) = stages 1+2 fused (S12), then stage 3.  Other values:
+ * HSGN_EINVAL. */
 hsgn_status hsgn_set_fused_stages(hsgn_ctx* ctx, int32_t mode);
 int32_t hsgn_fused_stages(const hsgn_ctx* ctx);
 
@@ -203,14 +195,24 @@ hsgn_status hsgn_recorder_snapshot(const hsgn_recorder* r, int32_t k, double* ta
 
 /* The bare fused fixed-step pipeline used by the benchmark: `steps` BS3 steps
  * of size dt on (y, k1) in place (k1 must hold f(y) on entry; it holds f(y)
- * of the new state on return, FSAL).  Graph-captured.  Returns HSGN_EDEPTH
- * if any stage input had !(h > 0); *steps_done gets the completed count. */
+ * of the new state on return, FSAL).  The caller's buffers are the
+ * integrator's parity-0 pair (no copies for an even count).  Graph-captured
+ * (slab contexts capture their NCCL halo exchanges too).  Returns
+ * HSGN_EDEPTH if any stage input had !(h > 0); *steps_done gets the
+ * completed count.  hsgn_last_timing() gives the device ms of the whole call. */
 hsgn_status hsgn_bs3_fixed_steps(hsgn_ctx* ctx, hsgn_state* y, hsgn_state* k1, double t, double dt,
                                  int64_t steps, int64_t* steps_done);
 /* Builds (captures and instantiates) the CUDA graphs that
- * hsgn_bs3_fixed_steps(ctx, ..., dt, steps, ...) will launch, without running
- * a step: graph construction is one-time host work, kept out of a timed run. */
-hsgn_status hsgn_prepare_fixed_steps(hsgn_ctx* ctx, double dt, int64_t steps);
+ * hsgn_bs3_fixed_steps(ctx, y, k1, ..., dt, steps, ...) will launch, without
+ * running a step: graph construction is one-time host work, kept out of a
+ * timed run. */
+hsgn_status hsgn_prepare_fixed_steps(hsgn_ctx* ctx, hsgn_state* y, hsgn_state* k1, double dt, int64_t steps);
+/* Per-kernel timing of the fixed-step graphs (whole-grid S12 + S3 contexts):
+ * with it on, the captured graphs carry CUDA event nodes around every
+ * kernel, and hsgn_kernel_times() returns the mean S12 and S3 durations of
+ * the last hsgn_bs3_fixed_steps call (measured inside that call). */
+hsgn_status hsgn_set_kernel_timing(hsgn_ctx* ctx, int32_t on);
+hsgn_status hsgn_kernel_times(const hsgn_ctx* ctx, double* s12_ms, double* s3_ms, int64_t* steps);
 
 /* ------------------------------------------------------------ diagnostics */
 
@@ -236,8 +238,8 @@ double hsgn_outer_sum(const hsgn_grid* grid, const double* rows, int32_t j_begin
 hsgn_status hsgn_profile_stages(hsgn_ctx* ctx, const hsgn_state* y, const hsgn_state* k1, double dt,
                                 int32_t reps, double* ms3);
 
-/* Mean device ms of the fused kernel of the current mode (S31 in mode 1,
- * the whole-step kernel in mode 2, S12 in mode 3) over `reps` launches. */
+/* Mean device ms of the fused S12 kernel over `reps` launches (inputs
+ * copied, caller state intact). */
 hsgn_status hsgn_profile_fused(hsgn_ctx* ctx, const hsgn_state* y, const hsgn_state* k1, double dt, int32_t reps,
                                double* ms);
 
@@ -292,6 +294,10 @@ const char* hsgn_scenario_name(int32_t k); /* scenario_names(), scenarios.hpp:70
 hsgn_status hsgn_scenario_make(const char* name, const char* const* keys, const double* vals, int32_t n,
                                hsgn_scenario* out, char* err, int32_t err_len);
 hsgn_status hsgn_scenario_sample(const hsgn_scenario* s, int32_t nx, int32_t ny, double* b, double* q5);
+/* The same for global rows [j0, j1) of the nx x ny grid only (a slab's
+ * rows; b and q5 hold (j1 - j0) * nx nodes per field). */
+hsgn_status hsgn_scenario_sample_rows(const hsgn_scenario* s, int32_t nx, int32_t ny, int32_t j0, int32_t j1,
+                                      double* b, double* q5);
 hsgn_status hsgn_scenario_exact(const hsgn_scenario* s, int32_t nx, int32_t ny, double t, double* q5);
 /* The spec's closed forms at one point: bhuv = {b, h0, u0, v0}(x, y). */
 hsgn_status hsgn_scenario_eval(const hsgn_scenario* s, double x, double y, double bhuv[4]);

@@ -10,6 +10,7 @@
 // oracle/_ref/libhsgn_ref.so is git-ignored and travels to the GPU box as a
 // prebuilt file.  Never linked by the product library.
 
+#include <random>
 #include <hsgn/analysis.hpp>
 #include <hsgn/config.hpp>
 #include <hsgn/io.hpp>
@@ -99,6 +100,24 @@ IntegratorConfig cfg_of(const orc_cfg* c) {
 extern "C" {
 
 void ref_set_threads(int n) { set_thread_count(n); }  // threading.hpp:12
+
+// The 300 random states of acceptance gate c2 (acceptance_main.cpp:88-127),
+// drawn exactly as the gate draws them: one std::mt19937(20260822) stream,
+// pos = U(0.5, 1.5), sym = U(-1, 1), per setup and trial the fields h (pos),
+// u, v, w (sym), eta (pos) of a 32 x 32 grid in storage order (libstdc++
+// streams, so the device tests get the reference's own inputs).
+// out: n_setups * trials * 5 * 1024 doubles.
+void ref_c2_states(int n_setups, int trials, double* out) {
+    std::mt19937 rng(20260822u);
+    std::uniform_real_distribution<double> pos(0.5, 1.5), sym(-1.0, 1.0);
+    const int n = 32 * 32;
+    for (int s = 0; s < n_setups; ++s)
+        for (int t = 0; t < trials; ++t)
+            for (int f = 0; f < 5; ++f) {
+                const bool positive = f == 0 || f == 4;
+                for (int k = 0; k < n; ++k) *out++ = positive ? pos(rng) : sym(rng);
+            }
+}
 int ref_max_threads(void) { return max_thread_count(); }
 
 void ref_default_cfg(orc_cfg* c) {

@@ -7,7 +7,7 @@ See DESIGN.md for the kernel design and INTEGRATION.md for the C ABI.
 from .api import (AcceptObserver, BoundaryKind, DepthError, DeviceState, Grid2D, HsgnError,
                   IntegratorConfig, PhysSetup, RhsContext, SolutionRecord, StateField, adaptive_solve,
                   bs3_fixed_steps, direction_spacing, discrete_l2_error, energy_rate, eoc, init_auxiliary,
-                  make_grid, make_rhs_context, mass_weighted_sum, prepare_fixed_steps, rhs, rhs_periodic, rhs_reflecting, rhs_shallow_water,
+                  make_grid, make_rhs_context, mass_weighted_sum, prepare_fixed_steps, kernel_times, set_kernel_timing, rhs, rhs_periodic, rhs_reflecting, rhs_shallow_water,
                   total_energy, total_mass)
 from .recorder import RunRecorder
 
@@ -15,6 +15,6 @@ __all__ = [
     "AcceptObserver", "BoundaryKind", "DepthError", "DeviceState", "Grid2D", "HsgnError", "IntegratorConfig",
     "PhysSetup", "RhsContext", "SolutionRecord", "StateField", "adaptive_solve", "bs3_fixed_steps",
     "direction_spacing", "discrete_l2_error", "energy_rate", "eoc", "init_auxiliary", "make_grid",
-    "make_rhs_context", "mass_weighted_sum", "prepare_fixed_steps", "rhs", "rhs_periodic", "rhs_reflecting", "rhs_shallow_water", "total_energy",
+    "make_rhs_context", "mass_weighted_sum", "prepare_fixed_steps", "kernel_times", "set_kernel_timing", "rhs", "rhs_periodic", "rhs_reflecting", "rhs_shallow_water", "total_energy",
     "total_mass", "RunRecorder",
 ]

@@ -84,8 +84,6 @@ def lib() -> C.CDLL:
     f("hsgn_set_rows_per_block", C.c_int, CTX, I32)
     f("hsgn_set_stencil_kind", C.c_int, CTX, I32)
     f("hsgn_stencil_kind", I32, CTX)
-    f("hsgn_set_tma", C.c_int, CTX, I32)
-    f("hsgn_tma_enabled", I32, CTX)
     f("hsgn_set_fused_stages", C.c_int, CTX, I32)
     f("hsgn_fused_stages", I32, CTX)
     f("hsgn_profile_fused", C.c_int, CTX, STATE, STATE, D, I32, PD)
@@ -101,7 +99,9 @@ def lib() -> C.CDLL:
     f("hsgn_init_auxiliary", C.c_int, CTX, STATE)
     f("hsgn_solve", C.c_int, CTX, STATE, D, D, CF, STATE, RC, OBSERVER, C.c_void_p)
     f("hsgn_bs3_fixed_steps", C.c_int, CTX, STATE, STATE, D, D, I64, C.POINTER(I64))
-    f("hsgn_prepare_fixed_steps", C.c_int, CTX, D, I64)
+    f("hsgn_prepare_fixed_steps", C.c_int, CTX, STATE, STATE, D, I64)
+    f("hsgn_set_kernel_timing", C.c_int, CTX, I32)
+    f("hsgn_kernel_times", C.c_int, CTX, PD, PD, C.POINTER(I64))
     f("hsgn_total_mass", C.c_int, CTX, STATE, PD)
     f("hsgn_total_energy", C.c_int, CTX, STATE, PD)
     f("hsgn_energy_rate", C.c_int, CTX, STATE, STATE, PD)
@@ -138,6 +138,7 @@ def lib() -> C.CDLL:
     f("hsgn_scenario_name", C.c_char_p, I32)
     f("hsgn_scenario_make", C.c_int, C.c_char_p, C.POINTER(C.c_char_p), PD, I32, SC, C.c_char_p, I32)
     f("hsgn_scenario_sample", C.c_int, SC, I32, I32, PD, PD)
+    f("hsgn_scenario_sample_rows", C.c_int, SC, I32, I32, I32, I32, PD, PD)
     f("hsgn_scenario_exact", C.c_int, SC, I32, I32, D, PD)
     f("hsgn_scenario_eval", C.c_int, SC, D, D, PD)
     _lib = L
@@ -148,7 +149,7 @@ def lib() -> C.CDLL:
 EXPORTS = [
     "hsgn_ctx_create", "hsgn_ctx_create_slab", "hsgn_nccl_unique_id", "hsgn_ctx_attach_nccl",
     "hsgn_ctx_destroy", "hsgn_last_error", "hsgn_set_source", "hsgn_set_rows_per_block",
-    "hsgn_set_stencil_kind", "hsgn_stencil_kind", "hsgn_set_tma", "hsgn_tma_enabled", "hsgn_n_evals",
+    "hsgn_set_stencil_kind", "hsgn_stencil_kind", "hsgn_n_evals",
     "hsgn_state_alloc", "hsgn_state_free", "hsgn_state_upload", "hsgn_state_download", "hsgn_state_copy",
     "hsgn_state_field_ptr", "hsgn_rhs", "hsgn_rhs_shallow_water", "hsgn_init_auxiliary", "hsgn_solve",
     "hsgn_bs3_fixed_steps", "hsgn_total_mass", "hsgn_total_energy", "hsgn_energy_rate",
@@ -162,4 +163,5 @@ EXPORTS = [
     "hsgn_set_fused_stages", "hsgn_fused_stages", "hsgn_profile_fused",
     "hsgn_scenario_count", "hsgn_scenario_name", "hsgn_scenario_make", "hsgn_scenario_sample",
     "hsgn_scenario_exact", "hsgn_prepare_fixed_steps", "hsgn_scenario_eval",
+    "hsgn_set_kernel_timing", "hsgn_kernel_times", "hsgn_scenario_sample_rows",
 ]

@@ -269,18 +269,9 @@ class RhsContext:
         _check(self, N.lib().hsgn_set_stencil_kind(self._h, int(kind)), "hsgn_set_stencil_kind")
 
     @property
-    def tma(self) -> bool:
-        """Raw inputs staged by TMA bulk copies (True) or register prefetch."""
-        return bool(N.lib().hsgn_tma_enabled(self._h))
-
-    @tma.setter
-    def tma(self, on: bool):
-        _check(self, N.lib().hsgn_set_tma(self._h, int(bool(on))), "hsgn_set_tma")
-
-    @property
     def fused_stages(self) -> int:
-        """Fixed-step kernel structure: 0 per stage, 1 stage 3 fused with the
-        next stage 1 (S31), 2 one kernel per whole step."""
+        """Fixed-step / attempt kernel structure: 0 one kernel per stage,
+        3 (default) stages 1 + 2 fused (S12), then stage 3."""
         return int(N.lib().hsgn_fused_stages(self._h))
 
     @fused_stages.setter
@@ -477,10 +468,25 @@ def adaptive_solve(ctx: RhsContext, q0, t0: float, t_final: float, cfg: Integrat
     return res
 
 
-def prepare_fixed_steps(ctx: RhsContext, dt: float, steps: int) -> None:
-    """Build the CUDA graphs bs3_fixed_steps(ctx, ..., dt, steps) will launch
-    (one-time host work; no step is run)."""
-    _check(ctx, N.lib().hsgn_prepare_fixed_steps(ctx._h, float(dt), int(steps)), "prepare_fixed_steps")
+def prepare_fixed_steps(ctx: RhsContext, y: DeviceState, k1: DeviceState, dt: float, steps: int) -> None:
+    """Build the CUDA graphs bs3_fixed_steps(ctx, y, k1, ..., dt, steps) will
+    launch (one-time host work; no step is run)."""
+    _check(ctx, N.lib().hsgn_prepare_fixed_steps(ctx._h, y._h, k1._h, float(dt), int(steps)),
+           "prepare_fixed_steps")
+
+
+def set_kernel_timing(ctx: RhsContext, on: bool) -> None:
+    """Event nodes around every kernel of the fixed-step graphs (whole grid,
+    S12 + S3): kernel_times() then gives the per-kernel durations measured
+    inside the last bs3_fixed_steps call."""
+    _check(ctx, N.lib().hsgn_set_kernel_timing(ctx._h, int(bool(on))), "set_kernel_timing")
+
+
+def kernel_times(ctx: RhsContext):
+    """(mean S12 ms, mean S3 ms, steps timed) of the last bs3_fixed_steps."""
+    a, b, n = C.c_double(0.0), C.c_double(0.0), C.c_int64(0)
+    _check(ctx, N.lib().hsgn_kernel_times(ctx._h, C.byref(a), C.byref(b), C.byref(n)), "kernel_times")
+    return a.value, b.value, n.value
 
 
 def bs3_fixed_steps(ctx: RhsContext, y: DeviceState, k1: DeviceState, t: float, dt: float, steps: int):

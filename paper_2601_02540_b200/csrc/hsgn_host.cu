@@ -27,6 +27,7 @@
 namespace hsgn_dev {
 // sgn_stage.cu
 cudaError_t launch_stage(int mode, const StageArgs& A, cudaStream_t st);
+int stage_launches(int mode, const StageArgs& A);
 int stage_grid_blocks(const StageArgs& A);
 cudaError_t launch_sum_partials(const double* part, int n, double* out, cudaStream_t st);
 // sgn_aux.cu
@@ -113,6 +114,7 @@ namespace {
 struct FixedGraph {
     cudaGraphExec_t exec = nullptr;
     int steps = 0;
+    int64_t kernels = 0;  // kernel nodes of this library in the graph
 };
 
 }  // namespace
@@ -120,6 +122,8 @@ struct FixedGraph {
 struct hsgn_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t cstream = nullptr;  // high-priority comm stream of an NCCL slab (halos, agreement)
+    cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_c = nullptr, ev_d = nullptr, ev_e = nullptr;  // slab schedule
     // global grid + slab
     hsgn_grid grid{};
     hsgn_phys phys{};
@@ -133,11 +137,11 @@ struct hsgn_ctx {
     int source = 0;
     int rows_per_block = 0;
     int forced_kind = -1;  // stencil kind override (tests); -1 = automatic
-    int use_tma = 0;       // TMA staging of raw inputs when nx is even (opt-in: slower in r1)
     int in_group = 0;      // member of an in-process slab group (halo pulls by the group)
     int ring1 = 0;         // 1-slab ring: NCCL attached to a 1-rank periodic-y context (halos to itself)
-    int fused = 3;         // fixed-step graphs (whole-grid contexts): 0 per stage, 1 S31, 2 whole step, 3 S12 + S3
+    int fused = 3;         // fixed-step structure: 0 one kernel per stage, 3 S12 + S3
     int64_t n_evals = 0;
+    int64_t launches = 0;  // kernels of this library launched (or captured) on the context stream
     std::string err;
     // workspace for the integrator
     hsgn_state ws[8];  // y0,y1,k1a,k1b,k2,part,scratchA,scratchB
@@ -151,7 +155,16 @@ struct hsgn_ctx {
     double* d_rows = nullptr;
     double* h_rows = nullptr;
     StepRec* h_rec = nullptr;
-    std::map<std::tuple<int, int, uint64_t, uint64_t, uint64_t, uint64_t>, FixedGraph> graphs;  // (steps, parity, gauges, dt, rpb, floor)
+    // fixed-step graphs by (steps, parity, recorder id, dt, rows per block, floor, y, k1, kernel timing)
+    std::map<std::tuple<int, int, uint64_t, uint64_t, uint64_t, uint64_t, const void*, const void*, int>, FixedGraph>
+        graphs;
+    // per-kernel timing of the fixed-step chunks (whole grid, S12 + S3): event
+    // nodes around every kernel of the captured graphs; the host accumulates
+    // the S12 and S3 durations after each chunk
+    int ktiming = 0;
+    std::vector<cudaEvent_t> kev;  // 3 per step + 1
+    double kt_ms[2] = {0.0, 0.0};  // summed S12, S3 ms
+    int64_t kt_n = 0;              // steps timed
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     double last_ms = 0.0;
     int64_t last_kernels = 0;
@@ -165,6 +178,7 @@ struct hsgn_ctx {
 // stride, snapshots are stream-ordered D2H copies into pinned memory.
 struct hsgn_recorder {
     hsgn_ctx* c = nullptr;
+    uint64_t id = 0;  // unique per recorder: keys the gauge-sampling graphs (never a reused address)
     std::vector<int32_t> gi, gj;
     std::vector<double> gx, gy;
     long long* d_idx = nullptr;  // j*nx + i per gauge
@@ -303,7 +317,6 @@ static hsgn_status setup_ctx(hsgn_ctx* c) {
     const bool cf = p2 && A.cpx == A.cpy && !A.x_bounded && A.y_lo != YE_CLAMP && A.y_hi != YE_CLAMP && !A.walls;
     A.pow2 = cf ? 2 : (p2 ? 1 : 0);
     if (c->forced_kind >= 0 && c->forced_kind < A.pow2) A.pow2 = c->forced_kind;
-    A.tma = c->use_tma && (g.nx % 2 == 0);
     A.g = c->phys.g;
     A.lambda = c->phys.lambda;
     A.lam_half = c->phys.lambda / 2.0;
@@ -352,7 +365,7 @@ static hsgn_status setup_ctx(hsgn_ctx* c) {
 // GHOST rows to rank+1; receive into our rows -GHOST..-1 / ny_loc..ny_loc+
 // GHOST-1.  One grouped NCCL call per exchange, on the context stream
 // (graph-capturable).
-static hsgn_status exchange(hsgn_ctx* c, const hsgn_state* s, int nfields) {
+static hsgn_status exchange_on(hsgn_ctx* c, const hsgn_state* s, int nfields, cudaStream_t stream) {
     if ((c->nranks == 1 && !c->ring1) || c->in_group) return HSGN_OK;  // in a group the driver pulls halos
     if (!c->comm) return fail(c, HSGN_ENCCL, "slab context has no NCCL communicator attached");
     const NcclApi& N = nccl();
@@ -369,14 +382,18 @@ static hsgn_status exchange(hsgn_ctx* c, const hsgn_state* s, int nfields) {
     int r = N.group_start();
     for (int f = 0; f < nfields && r == 0; ++f) {
         double* fld = s->f(f);
-        if (up >= 0) r |= N.send(fld + (long long)(c->ny_loc - GHOST) * nx, span, NCCL_FLOAT64, up, c->comm, c->stream);
-        if (dn >= 0) r |= N.recv(fld - span, span, NCCL_FLOAT64, dn, c->comm, c->stream);
-        if (dn >= 0) r |= N.send(fld, span, NCCL_FLOAT64, dn, c->comm, c->stream);
-        if (up >= 0) r |= N.recv(fld + (long long)c->ny_loc * nx, span, NCCL_FLOAT64, up, c->comm, c->stream);
+        if (up >= 0) r |= N.send(fld + (long long)(c->ny_loc - GHOST) * nx, span, NCCL_FLOAT64, up, c->comm, stream);
+        if (dn >= 0) r |= N.recv(fld - span, span, NCCL_FLOAT64, dn, c->comm, stream);
+        if (dn >= 0) r |= N.send(fld, span, NCCL_FLOAT64, dn, c->comm, stream);
+        if (up >= 0) r |= N.recv(fld + (long long)c->ny_loc * nx, span, NCCL_FLOAT64, up, c->comm, stream);
     }
     r |= N.group_end();
     if (r) return fail(c, HSGN_ENCCL, "ncclSend/Recv halo exchange failed (%d)", r);
     return HSGN_OK;
+}
+
+static hsgn_status exchange(hsgn_ctx* c, const hsgn_state* s, int nfields) {
+    return exchange_on(c, s, nfields, c->stream);
 }
 
 // Cross-rank agreement of a P-rank decomposition.  Every decision the
@@ -387,22 +404,22 @@ static hsgn_status exchange(hsgn_ctx* c, const hsgn_state* s, int nfields) {
 // context stream before the host reads them (graph-capturable, no host sync).
 static bool multi_rank(const hsgn_ctx* c) { return c->nranks > 1 && !c->in_group; }
 
-static hsgn_status agree(hsgn_ctx* c, void* d, size_t count, int dtype, int op) {
+static hsgn_status agree(hsgn_ctx* c, void* d, size_t count, int dtype, int op, cudaStream_t stream = nullptr) {
     if (!multi_rank(c)) return HSGN_OK;
     if (!c->comm) return fail(c, HSGN_ENCCL, "slab context has no NCCL communicator attached");
-    const int r = nccl().allreduce(d, d, count, dtype, op, c->comm, c->stream);
+    const int r = nccl().allreduce(d, d, count, dtype, op, c->comm, stream ? stream : c->stream);
     if (r) return fail(c, HSGN_ENCCL, "ncclAllReduce failed (%d)", r);
     return HSGN_OK;
 }
 
 // A step record: depth-failure counts summed, min(ynew.h) bit pattern
 // min-reduced (positive doubles order as their bit patterns), one NCCL group.
-static hsgn_status agree_rec(hsgn_ctx* c, StepRec* rec) {
+static hsgn_status agree_rec(hsgn_ctx* c, StepRec* rec, cudaStream_t stream = nullptr) {
     if (!multi_rank(c) || !rec) return HSGN_OK;
     const NcclApi& N = nccl();
     int r = N.group_start();
-    hsgn_status s = agree(c, rec->bad, 3, NCCL_UINT64, NCCL_SUM);
-    if (!s) s = agree(c, &rec->minh, 1, NCCL_UINT64, NCCL_MIN);
+    hsgn_status s = agree(c, rec->bad, 3, NCCL_UINT64, NCCL_SUM, stream);
+    if (!s) s = agree(c, &rec->minh, 1, NCCL_UINT64, NCCL_MIN, stream);
     r |= N.group_end();
     if (s) return s;
     if (r) return fail(c, HSGN_ENCCL, "ncclGroupEnd failed (%d)", r);
@@ -421,6 +438,13 @@ static StageArgs stage_args(hsgn_ctx* c, int mode, double t) {
 
 static hsgn_status launch(hsgn_ctx* c, int mode, const StageArgs& A) {
     CK(launch_stage(mode, A, c->stream));
+    c->launches += stage_launches(mode, A);
+    return HSGN_OK;
+}
+
+static hsgn_status gauges_launch(hsgn_ctx* c, const hsgn_state* q, const hsgn_recorder* R, int row) {
+    CK(launch_gauges(q->base, c->b, R->d_idx, (int)R->gi.size(), R->d_gauge + (size_t)row * R->gi.size(), c->stream));
+    ++c->launches;
     return HSGN_OK;
 }
 
@@ -472,18 +496,6 @@ static hsgn_status enqueue_stage(hsgn_ctx* c, int stage, const hsgn_state* y, co
                                  hsgn_state* ynew, hsgn_state* k4, hsgn_state* part, StepRec* rec,
                                  const StepRec* prev, double t, double dt, bool adaptive, double atol,
                                  double rtol) {
-    if (stage == 31) {  // fused: k4 = f(ynew) of this step, k2 = f(ynew + dt/2 k4) of the next (rec = next's)
-        StageArgs A = stage_args(c, MODE_S31, t + dt);
-        A.a = 0.5 * dt;
-        A.y = ynew->base;
-        A.out = k4->base;
-        A.out2 = k2->base;
-        A.bad = const_cast<unsigned long long*>(&prev->bad[2]);  // the S3 half belongs to the previous step
-        A.bad2 = &rec->bad[0];
-        A.halt = c->d_halt;
-        A.chk_bad = &prev->bad[1];
-        return launch(c, MODE_S31, A);
-    }
     StageArgs A;
     if (stage == 1) {  // k2 = f(t + dt/2, y + (dt/2) k1)
         A = stage_args(c, MODE_S1, t + 0.5 * dt);
@@ -493,7 +505,8 @@ static hsgn_status enqueue_stage(hsgn_ctx* c, int stage, const hsgn_state* y, co
         A.out = k2->base;
         A.bad = &rec->bad[0];
         A.halt = c->d_halt;
-        A.chk_bad = prev ? &prev->bad[2] : nullptr;
+        if (prev)  // the previous step's (agreed) record: any stage failure or the floor
+            for (int k = 0; k < 3; ++k) A.chk_bad[k] = &prev->bad[k];
         A.chk_minh = prev ? &prev->minh : nullptr;
         return launch(c, MODE_S1, A);
     }
@@ -511,7 +524,8 @@ static hsgn_status enqueue_stage(hsgn_ctx* c, int stage, const hsgn_state* y, co
         A.err_part = c->d_err_part;
         A.bad = &rec->bad[2];
         A.halt = c->d_halt;
-        A.chk_bad = &rec->bad[1];
+        A.chk_bad[0] = &rec->bad[0];
+        A.chk_bad[1] = &rec->bad[1];
         return launch(c, MODE_S3, A);
     }
     // stage 2: k3 = f(t + 3dt/4, y + (3dt/4) k2); ynew = y + (2/9 dt) k1 + (1/3 dt) k2 + (4/9 dt) k3
@@ -533,68 +547,18 @@ static hsgn_status enqueue_stage(hsgn_ctx* c, int stage, const hsgn_state* y, co
     A.bad = &rec->bad[1];
     A.minh = &rec->minh;
     A.halt = c->d_halt;
-    A.chk_bad = &rec->bad[0];
-    if (prev && c->fused) {  // after an S31: its S3 half and the floor of the previous step
-        A.chk_bad2 = &prev->bad[2];
-        A.chk_minh = &prev->minh;
-    }
+    A.chk_bad[0] = &rec->bad[0];
     return launch(c, MODE_S2, A);
 }
 
-// One whole fixed step (STEP kernel): y, k1 -> ynew, k4 with the records of
-// step `rec` (prev: the previous step's, for the halt test).
-static hsgn_status enqueue_step_kernel(hsgn_ctx* c, const hsgn_state* y, const hsgn_state* k1, hsgn_state* ynew,
-                                       hsgn_state* k4, StepRec* rec, const StepRec* prev, double dt) {
-    StageArgs A = stage_args(c, MODE_STEP, 0.0);
-    A.a = 0.5 * dt;
-    A.a2 = 0.75 * dt;
-    A.c1 = dt * (2.0 / 9.0);
-    A.c2 = dt * (1.0 / 3.0);
-    A.c3 = dt * (4.0 / 9.0);
-    A.y = y->base;
-    A.k = k1->base;
-    A.out = ynew->base;
-    A.out2 = k4->base;
-    A.bad = &rec->bad[0];
-    A.bad2 = &rec->bad[1];
-    A.bad3 = &rec->bad[2];
-    A.minh = &rec->minh;
-    A.halt = c->d_halt;
-    if (prev) {
-        A.chk_bad = &prev->bad[0];
-        A.chk_bad2 = &prev->bad[1];
-        A.chk_bad3 = &prev->bad[2];
-        A.chk_minh = &prev->minh;
-    }
-    return launch(c, MODE_STEP, A);
-}
-
-// A chunk of `steps` fixed steps, one STEP kernel each (+1 gauge gather per
-// step with a recorder).  Whole-grid contexts.
-static hsgn_status enqueue_chunk_step(hsgn_ctx* c, int parity, int steps, double dt, const hsgn_recorder* R) {
-    hsgn_state* Y[2] = {&c->ws[0], &c->ws[1]};
-    hsgn_state* K[2] = {&c->ws[2], &c->ws[3]};
-    const bool gauges = R && !R->gi.empty();
-    hsgn_status st;
-    for (int s = 0; s < steps; ++s) {
-        const int p = (parity + s) & 1;
-        if ((st = enqueue_step_kernel(c, Y[p], K[p], Y[p ^ 1], K[p ^ 1], &c->d_rec[s], s ? &c->d_rec[s - 1] : nullptr,
-                                      dt)))
-            return st;
-        if (gauges)
-            CK(launch_gauges(Y[p ^ 1]->base, c->b, R->d_idx, (int)R->gi.size(),
-                             R->d_gauge + (size_t)s * R->gi.size(), c->stream));
-    }
-    return HSGN_OK;
-}
-
-// A chunk of `steps` fixed steps as S12 (stages 1+2) + S3 per step.
-// One fixed step as S12 (stages 1+2: y, k1 -> ynew) then S3 (k4 = f(ynew)),
-// each followed by the slab halo exchange of its output (no-op on a whole
-// grid; in an in-process group the driver pulls instead: pass `group`).
+// One fixed step as S12 (stages 1+2: y, k1 -> ynew) then S3 (k4 = f(ynew)).
+// Rows [band0, band1) of the slab only (band1 == 0: all rows).
 static hsgn_status enqueue_s12(hsgn_ctx* c, const hsgn_state* y, const hsgn_state* k1, hsgn_state* ynew,
-                               StepRec* rec, const StepRec* prev, double dt, hsgn_state* part = nullptr) {
+                               StepRec* rec, const StepRec* prev, double dt, hsgn_state* part = nullptr,
+                               int band0 = 0, int band1 = 0) {
     StageArgs A = stage_args(c, MODE_S12, 0.0);
+    A.band0 = band0;
+    A.band1 = band1;
     A.a = 0.5 * dt;
     A.a2 = 0.75 * dt;
     A.c1 = dt * (2.0 / 9.0);
@@ -607,7 +571,11 @@ static hsgn_status enqueue_s12(hsgn_ctx* c, const hsgn_state* y, const hsgn_stat
     A.bad2 = &rec->bad[1];
     A.minh = &rec->minh;
     A.halt = c->d_halt;
-    A.chk_bad = prev ? &prev->bad[2] : nullptr;
+    // halt on the previous step's record: with a P-rank decomposition it is
+    // the agreed one, so every rank stops at the same step even when a
+    // stage-1 / stage-2 failure was local to another rank
+    if (prev)
+        for (int k = 0; k < 3; ++k) A.chk_bad[k] = &prev->bad[k];
     A.chk_minh = prev ? &prev->minh : nullptr;
     if (part) {  // adaptive attempt: error partials for the adaptive S3
         A.adaptive = 1;
@@ -619,89 +587,139 @@ static hsgn_status enqueue_s12(hsgn_ctx* c, const hsgn_state* y, const hsgn_stat
     return launch(c, MODE_S12, A);
 }
 
-static hsgn_status enqueue_s3_fixed(hsgn_ctx* c, const hsgn_state* ynew, hsgn_state* k4, StepRec* rec, double dt) {
+static hsgn_status enqueue_s3_fixed(hsgn_ctx* c, const hsgn_state* ynew, hsgn_state* k4, StepRec* rec, double dt,
+                                    int band0 = 0, int band1 = 0) {
     StageArgs A = stage_args(c, MODE_S3, dt);  // k4 = f(ynew), FSAL
+    A.band0 = band0;
+    A.band1 = band1;
     A.y = ynew->base;
     A.out = k4->base;
     A.bad = &rec->bad[2];
     A.halt = c->d_halt;
-    A.chk_bad = &rec->bad[1];
-    A.chk_bad2 = &rec->bad[0];
+    A.chk_bad[0] = &rec->bad[0];
+    A.chk_bad[1] = &rec->bad[1];
     return launch(c, MODE_S3, A);
 }
 
-// A chunk of `steps` fixed steps as S12 + S3 per step (+1 gauge gather per
-// step with a recorder; slab halo exchanges after each kernel).
-static hsgn_status enqueue_chunk_s12(hsgn_ctx* c, int parity, int steps, double dt, const hsgn_recorder* R) {
-    hsgn_state* Y[2] = {&c->ws[0], &c->ws[1]};
-    hsgn_state* K[2] = {&c->ws[2], &c->ws[3]};
-    const bool gauges = R && !R->gi.empty();
+// The integrator's double-buffered fixed-step state: step s reads (Y[p],
+// K[p]) and writes (Y[p^1], K[p^1]), p = (parity + s) & 1.
+struct Bufs {
+    hsgn_state* Y[2];
+    hsgn_state* K[2];
+};
+
+static Bufs ws_bufs(hsgn_ctx* c) { return Bufs{{&c->ws[0], &c->ws[1]}, {&c->ws[2], &c->ws[3]}}; }
+
+#define CKE(call)                                                                              \
+    do {                                                                                       \
+        cudaError_t e_ = (call);                                                               \
+        if (e_ != cudaSuccess) return fail(c, HSGN_ECUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+    } while (0)
+
+// Overlapped slab step: the rows that feed or need
+// ghost rows run as separate edge-band launches, the halo exchanges and the
+// step agreement run on the high-priority comm stream while the interior
+// band computes.  Stream C (context stream):
+//   S12[0,G) S12[ny-G,ny) -evA-  S12[G,ny-G)  (wait evB) S3[0,G) S3[ny-G,ny) -evC-  S3[G,ny-G) -evE-
+// stream M:  (wait evA) exchange ynew -evB-  (wait evC) exchange k4  (wait evE) agree(rec) -evD-
+// and the next step's first kernel waits evD (its ghost rows and the agreed
+// record).  G = GHOST: the exchanged boundary rows of ynew are written by
+// the S12 edge bands and those of k4 by the S3 edge bands, so the interior
+// launches never touch a row in flight.
+static hsgn_status enqueue_slab_step(hsgn_ctx* c, const Bufs& B, int p, StepRec* rec, const StepRec* prev,
+                                     double dt) {
+    const int ny = c->ny_loc, G = GHOST;
+    hsgn_state *y = B.Y[p], *k1 = B.K[p], *yn = B.Y[p ^ 1], *k4 = B.K[p ^ 1];
     hsgn_status st;
-    for (int s = 0; s < steps; ++s) {
-        const int p = (parity + s) & 1;
-        StepRec* rec = &c->d_rec[s];
-        if ((st = enqueue_s12(c, Y[p], K[p], Y[p ^ 1], rec, s ? &c->d_rec[s - 1] : nullptr, dt))) return st;
-        if ((st = exchange(c, Y[p ^ 1], 5))) return st;
-        if (gauges)
-            CK(launch_gauges(Y[p ^ 1]->base, c->b, R->d_idx, (int)R->gi.size(),
-                             R->d_gauge + (size_t)s * R->gi.size(), c->stream));
-        if ((st = enqueue_s3_fixed(c, Y[p ^ 1], K[p ^ 1], rec, dt))) return st;
-        if ((st = exchange(c, K[p ^ 1], 5))) return st;
-        if ((st = agree_rec(c, rec))) return st;  // the next S12 halts on the global record
-    }
+    if (prev) CKE(cudaStreamWaitEvent(c->stream, c->ev_d, 0));
+    if ((st = enqueue_s12(c, y, k1, yn, rec, prev, dt, nullptr, 0, G))) return st;
+    if ((st = enqueue_s12(c, y, k1, yn, rec, prev, dt, nullptr, ny - G, ny))) return st;
+    CKE(cudaEventRecord(c->ev_a, c->stream));
+    CKE(cudaStreamWaitEvent(c->cstream, c->ev_a, 0));
+    if ((st = exchange_on(c, yn, 5, c->cstream))) return st;
+    CKE(cudaEventRecord(c->ev_b, c->cstream));
+    if ((st = enqueue_s12(c, y, k1, yn, rec, prev, dt, nullptr, G, ny - G))) return st;
+    CKE(cudaStreamWaitEvent(c->stream, c->ev_b, 0));
+    if ((st = enqueue_s3_fixed(c, yn, k4, rec, dt, 0, G))) return st;
+    if ((st = enqueue_s3_fixed(c, yn, k4, rec, dt, ny - G, ny))) return st;
+    CKE(cudaEventRecord(c->ev_c, c->stream));
+    CKE(cudaStreamWaitEvent(c->cstream, c->ev_c, 0));
+    if ((st = exchange_on(c, k4, 5, c->cstream))) return st;
+    if ((st = enqueue_s3_fixed(c, yn, k4, rec, dt, G, ny - G))) return st;
+    CKE(cudaEventRecord(c->ev_e, c->stream));
+    CKE(cudaStreamWaitEvent(c->cstream, c->ev_e, 0));
+    if ((st = agree_rec(c, rec, c->cstream))) return st;  // all stage counters of this step are final
+    CKE(cudaEventRecord(c->ev_d, c->cstream));
     return HSGN_OK;
 }
 
-// A chunk of `steps` fixed steps from buffer parity `parity` with the fused
-// S3+S1 kernel between steps: S1, S2, (S31, S2) x (steps-1), S3 -- 2 steps+1
-// launches (+1 gauge gather per step with a recorder).  Whole-grid contexts.
-static hsgn_status enqueue_chunk_fused(hsgn_ctx* c, int parity, int steps, double dt, const hsgn_recorder* R,
-                                       int64_t* kernels) {
-    hsgn_state* Y[2] = {&c->ws[0], &c->ws[1]};
-    hsgn_state* K[2] = {&c->ws[2], &c->ws[3]};
-    hsgn_state* k2 = &c->ws[4];
+static bool slab_overlap(const hsgn_ctx* c) { return !whole(c) && !c->in_group && c->ny_loc >= 3 * GHOST; }
+
+// A chunk of `steps` fixed steps as S12 + S3 per step (+1 gauge gather per
+// step with a recorder).  Whole grid: two launches per step.  NCCL slab:
+// the overlapped schedule above, or (thin slabs) the exchanges serialised
+// after each kernel.
+static hsgn_status enqueue_chunk_s12(hsgn_ctx* c, const Bufs& B, int parity, int steps, double dt,
+                                     const hsgn_recorder* R) {
     const bool gauges = R && !R->gi.empty();
+    const bool overlap = slab_overlap(c);
     hsgn_status st;
     for (int s = 0; s < steps; ++s) {
         const int p = (parity + s) & 1;
         StepRec* rec = &c->d_rec[s];
         const StepRec* prev = s ? &c->d_rec[s - 1] : nullptr;
-        if (s == 0 && (st = enqueue_stage(c, 1, Y[p], K[p], k2, Y[p ^ 1], K[p ^ 1], nullptr, rec, nullptr, 0.0, dt,
-                                          false, 0, 0)))
-            return st;
-        if ((st = enqueue_stage(c, 2, Y[p], K[p], k2, Y[p ^ 1], K[p ^ 1], nullptr, rec, prev, 0.0, dt, false, 0, 0)))
-            return st;
-        if (gauges) {
-            CK(launch_gauges(Y[p ^ 1]->base, c->b, R->d_idx, (int)R->gi.size(),
-                             R->d_gauge + (size_t)s * R->gi.size(), c->stream));
-            if (kernels) ++*kernels;
+        if (overlap) {
+            if ((st = enqueue_slab_step(c, B, p, rec, prev, dt))) return st;
+            continue;
         }
-        if (s + 1 < steps)
-            st = enqueue_stage(c, 31, Y[p], K[p], k2, Y[p ^ 1], K[p ^ 1], nullptr, &c->d_rec[s + 1], rec, 0.0, dt,
-                               false, 0, 0);
-        else
-            st = enqueue_stage(c, 3, Y[p], K[p], k2, Y[p ^ 1], K[p ^ 1], nullptr, rec, prev, 0.0, dt, false, 0, 0);
-        if (st) return st;
+        const bool kt = c->ktiming && whole(c);
+        // (event record NODES of the captured graph: cudaEventRecordExternal)
+        if (kt) CKE(cudaEventRecordWithFlags(c->kev[3 * s], c->stream, cudaEventRecordExternal));
+        if ((st = enqueue_s12(c, B.Y[p], B.K[p], B.Y[p ^ 1], rec, prev, dt))) return st;
+        if (kt) CKE(cudaEventRecordWithFlags(c->kev[3 * s + 1], c->stream, cudaEventRecordExternal));
+        if ((st = exchange(c, B.Y[p ^ 1], 5))) return st;
+        if (gauges && (st = gauges_launch(c, B.Y[p ^ 1], R, s))) return st;
+        if (kt) CKE(cudaEventRecordWithFlags(c->kev[3 * s + 2], c->stream, cudaEventRecordExternal));
+        if ((st = enqueue_s3_fixed(c, B.Y[p ^ 1], B.K[p ^ 1], rec, dt))) return st;
+        if (kt && s + 1 == steps) CKE(cudaEventRecordWithFlags(c->kev[3 * steps], c->stream, cudaEventRecordExternal));
+        if ((st = exchange(c, B.K[p ^ 1], 5))) return st;
+        if ((st = agree_rec(c, rec))) return st;  // the next S12 halts on the global record
     }
-    if (kernels) *kernels += 2 * steps + 1;
+    if (overlap && steps > 0) CKE(cudaStreamWaitEvent(c->stream, c->ev_d, 0));  // join the comm stream
     return HSGN_OK;
 }
 
-// One fused BS3 step (S1, S2, S3) with the slab halo exchange after each
-// stage (k2, ynew, k4): DESIGN.md section 6.
+// One BS3 step as one kernel per stage (S1, S2, S3) with the slab halo
+// exchange after each stage (k2, ynew, k4): DESIGN.md section 6.
 static hsgn_status enqueue_step(hsgn_ctx* c, const hsgn_state* y, const hsgn_state* k1, hsgn_state* k2,
                                 hsgn_state* ynew, hsgn_state* k4, hsgn_state* part, StepRec* rec,
                                 const StepRec* prev, double t, double dt, bool adaptive, double atol,
-                                double rtol, int64_t* kernels) {
+                                double rtol) {
     hsgn_state* produced[3] = {k2, ynew, k4};
-    hsgn_status s0;
     for (int stage = 1; stage <= 3; ++stage) {
         hsgn_status s = enqueue_stage(c, stage, y, k1, k2, ynew, k4, part, rec, prev, t, dt, adaptive, atol, rtol);
         if (s) return s;
         if ((s = exchange(c, produced[stage - 1], 5))) return s;
     }
-    if ((s0 = agree_rec(c, rec))) return s0;
-    if (kernels) *kernels += 3;
+    return agree_rec(c, rec);
+}
+
+// A chunk of `steps` fixed steps, one kernel per stage (+ gauges); t is the
+// time of the first step (the source term needs it; graphs are built only
+// without a source).
+static hsgn_status enqueue_chunk_stages(hsgn_ctx* c, const Bufs& B, int parity, int steps, double t, double dt,
+                                        const hsgn_recorder* R) {
+    const bool gauges = R && !R->gi.empty();
+    hsgn_status st;
+    double ts = t;
+    for (int s = 0; s < steps; ++s) {
+        const int p = (parity + s) & 1;
+        if ((st = enqueue_step(c, B.Y[p], B.K[p], &c->ws[4], B.Y[p ^ 1], B.K[p ^ 1], nullptr, &c->d_rec[s],
+                               s ? &c->d_rec[s - 1] : nullptr, ts, dt, false, 0, 0)))
+            return st;
+        if (gauges && (st = gauges_launch(c, B.Y[p ^ 1], R, s))) return st;
+        ts = ts + dt;
+    }
     return HSGN_OK;
 }
 
@@ -732,6 +750,7 @@ static hsgn_status rhs_checked(hsgn_ctx* c, double t, const hsgn_state* q, hsgn_
     unsigned long long* d_bad = &c->d_rec[0].bad[0];
     CK(cudaMemsetAsync(d_bad, 0, sizeof(unsigned long long), c->stream));
     CK(launch_depth_check(q->base, (long long)c->ny_loc * c->grid.nx, d_bad, c->stream));
+    ++c->launches;
     if ((s = agree(c, d_bad, 1, NCCL_UINT64, NCCL_SUM))) return s;
     unsigned long long hb = 0;
     CK(cudaMemcpyAsync(&hb, d_bad, sizeof hb, cudaMemcpyDeviceToHost, c->stream));
@@ -813,6 +832,8 @@ static hsgn_status create_common(const hsgn_grid* grid, const hsgn_phys* phys, c
     if (grid->nx < 4 || grid->ny < 4) return bad_arg("make_grid: need at least 4 nodes per direction");
     if (nranks < 1 || rank < 0 || rank >= nranks || j_begin < 0 || j_end > grid->ny || j_end - j_begin < GHOST)
         return bad_arg("invalid slab");
+    if (nranks == 1 && (j_begin != 0 || j_end != grid->ny))  // one rank holds the whole grid
+        return bad_arg("invalid slab: a 1-rank decomposition must own rows [0, ny)");
     c->j_begin = j_begin;
     c->j_end = j_end;
     c->rank = rank;
@@ -878,6 +899,14 @@ hsgn_status hsgn_ctx_attach_nccl(hsgn_ctx* c, const unsigned char nccl_id[128]) 
     DeviceGuard dg_(c->device);
     int r = N.init_rank(&c->comm, c->nranks, id, c->rank);
     if (r) return fail(c, HSGN_ENCCL, "ncclCommInitRank failed (%d)", r);
+    if (!c->cstream) {  // the slab schedule's comm stream: highest priority, so its
+                        // NCCL kernels take the next free SM slots of a running interior launch
+        int lo = 0, hi = 0;
+        CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        CK(cudaStreamCreateWithPriority(&c->cstream, cudaStreamNonBlocking, hi));
+        for (cudaEvent_t* e : {&c->ev_a, &c->ev_b, &c->ev_c, &c->ev_d, &c->ev_e})
+            CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    }
     if (c->nranks == 1 && c->grid.kind_y != HSGN_BOUNDED && !c->ring1) {
         // a 1-rank periodic communicator: the context becomes a 1-slab ring
         // (ghost-row edges, halos sent to itself), i.e. exactly the P-rank
@@ -915,7 +944,11 @@ hsgn_status hsgn_ctx_destroy(hsgn_ctx* c) {
     if (c->h_rows) cudaFreeHost(c->h_rows);
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
+    for (cudaEvent_t e : c->kev) cudaEventDestroy(e);
     if (c->comm) nccl().destroy(c->comm);
+    for (cudaEvent_t e : {c->ev_a, c->ev_b, c->ev_c, c->ev_d, c->ev_e})
+        if (e) cudaEventDestroy(e);
+    if (c->cstream) cudaStreamDestroy(c->cstream);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
     return HSGN_OK;
@@ -962,20 +995,12 @@ hsgn_status hsgn_set_stencil_kind(hsgn_ctx* c, int32_t kind) {
 int32_t hsgn_stencil_kind(const hsgn_ctx* c) { return c ? c->base.pow2 : -1; }
 
 hsgn_status hsgn_set_fused_stages(hsgn_ctx* c, int32_t mode) {
-    if (!c || mode < 0 || mode > 3) return HSGN_EINVAL;
+    if (!c || (mode != 0 && mode != 3)) return HSGN_EINVAL;
     c->fused = mode;
     return reconfigure(c);
 }
 
 int32_t hsgn_fused_stages(const hsgn_ctx* c) { return c ? c->fused : 0; }
-
-hsgn_status hsgn_set_tma(hsgn_ctx* c, int32_t on) {
-    if (!c) return HSGN_EINVAL;
-    c->use_tma = on ? 1 : 0;
-    return reconfigure(c);
-}
-
-int32_t hsgn_tma_enabled(const hsgn_ctx* c) { return c ? c->base.tma : 0; }
 
 int64_t hsgn_n_evals(const hsgn_ctx* c) { return c ? c->n_evals : 0; }
 
@@ -1130,38 +1155,39 @@ uint64_t bits_of(double v) {
     return u;
 }
 
-// Capture (or fetch) a graph of `steps` fused steps starting at buffer parity
-// p; with a recorder that has gauges, each step also samples them (row s of
-// the staging block).
-hsgn_status get_fixed_graph(hsgn_ctx* c, int steps, int parity, double dt, const hsgn_recorder* R,
+// Enqueue a chunk of `steps` fixed steps on buffers B from parity `parity`
+// in the context's fixed-step structure (records reset first).
+hsgn_status enqueue_chunk(hsgn_ctx* c, const Bufs& B, int parity, int steps, double t, double dt,
+                          const hsgn_recorder* R) {
+    reset_recs(c, steps);
+    if (c->fused == 3 && c->source == 0) return enqueue_chunk_s12(c, B, parity, steps, dt, R);
+    return enqueue_chunk_stages(c, B, parity, steps, t, dt, R);
+}
+
+// Capture (or fetch) a graph of `steps` fixed steps on buffers B from parity
+// `parity`; with a recorder that has gauges, each step also samples them
+// (row s of the staging block).  Slab contexts capture their NCCL halo
+// exchanges, the step agreement and the comm-stream fork / join too.
+hsgn_status get_fixed_graph(hsgn_ctx* c, const Bufs& B, int steps, int parity, double dt, const hsgn_recorder* R,
                             FixedGraph** out) {
     const bool gauges = R && !R->gi.empty();
-    auto key = std::make_tuple(steps, parity, gauges ? (uint64_t)(uintptr_t)R->d_gauge : 0ull, bits_of(dt),
-                               (uint64_t)c->base.rows_per_block, bits_of(c->base.h_floor));
+    const int kt = c->ktiming && whole(c) && c->fused == 3;
+    auto key = std::make_tuple(steps, parity, gauges ? R->id : 0ull, bits_of(dt), (uint64_t)c->base.rows_per_block,
+                               bits_of(c->base.h_floor), (const void*)B.Y[0]->base, (const void*)B.K[0]->base, kt);
     auto it = c->graphs.find(key);
     if (it != c->graphs.end()) {
         *out = &it->second;
         return HSGN_OK;
     }
-    hsgn_state* Y[2] = {&c->ws[0], &c->ws[1]};
-    hsgn_state* K[2] = {&c->ws[2], &c->ws[3]};
     cudaGraph_t g = nullptr;
-    CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-    reset_recs(c, steps);
-    hsgn_status st = HSGN_OK;
-    if (c->fused == 1 && whole(c)) st = enqueue_chunk_fused(c, parity, steps, dt, R, nullptr);
-    if (c->fused == 2 && whole(c)) st = enqueue_chunk_step(c, parity, steps, dt, R);
-    if (c->fused == 3 && whole(c)) st = enqueue_chunk_s12(c, parity, steps, dt, R);
-    for (int s = 0; s < steps && !st && !(c->fused && whole(c)); ++s) {
-        const int p = (parity + s) & 1;
-        st = enqueue_step(c, Y[p], K[p], &c->ws[4], Y[p ^ 1], K[p ^ 1], nullptr, &c->d_rec[s],
-                          s ? &c->d_rec[s - 1] : nullptr, 0.0, dt, false, 0, 0, nullptr);
-        if (!st && gauges) {
-            cudaError_t ge = launch_gauges(Y[p ^ 1]->base, c->b, R->d_idx, (int)R->gi.size(),
-                                           R->d_gauge + (size_t)s * R->gi.size(), c->stream);
-            if (ge != cudaSuccess) st = fail(c, HSGN_ECUDA, "gauge launch: %s", cudaGetErrorString(ge));
-        }
+    const int64_t l0 = c->launches;
+    while (kt && (int)c->kev.size() < 3 * steps + 1) {
+        cudaEvent_t e;
+        CK(cudaEventCreate(&e));
+        c->kev.push_back(e);
     }
+    CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    hsgn_status st = enqueue_chunk(c, B, parity, steps, 0.0, dt, R);
     cudaError_t e = cudaStreamEndCapture(c->stream, &g);
     if (st) {
         if (g) cudaGraphDestroy(g);
@@ -1170,6 +1196,8 @@ hsgn_status get_fixed_graph(hsgn_ctx* c, int steps, int parity, double dt, const
     CK(e);
     FixedGraph fg;
     fg.steps = steps;
+    fg.kernels = c->launches - l0;
+    c->launches = l0;  // captured, not launched: counted when the graph runs
     e = cudaGraphInstantiate(&fg.exec, g, 0);
     cudaGraphDestroy(g);
     CK(e);
@@ -1180,51 +1208,34 @@ hsgn_status get_fixed_graph(hsgn_ctx* c, int steps, int parity, double dt, const
 
 }  // namespace
 
-// Fixed-step chunk runner: runs `steps` steps from (ws[p], ws[2+p]) without a
-// source term (graph) or with one (direct launches, t baked per step).
-// Returns the number of completed steps and the failure kind (0 none,
-// 1 depth at stage k (fail_stage), 2 floor).
-static hsgn_status run_fixed_chunk(hsgn_ctx* c, int parity, int steps, double t, double dt, int* done,
-                                   int* fail_kind, int* fail_stage, int64_t* kernels,
-                                   const hsgn_recorder* R = nullptr) {
-    const bool gauges = R && !R->gi.empty();
+// Fixed-step chunk runner: runs `steps` steps from (B.Y[parity],
+// B.K[parity]) without a source term (one CUDA graph) or with one (direct
+// launches, t baked per step).  Returns the number of completed steps and
+// the failure kind (0 none, 1 depth at stage k (fail_stage), 2 floor).
+static hsgn_status run_fixed_chunk(hsgn_ctx* c, const Bufs& B, int parity, int steps, double t, double dt,
+                                   int* done, int* fail_kind, int* fail_stage, const hsgn_recorder* R = nullptr) {
     hsgn_status st;
     if ((st = ensure_ws(c, steps))) return st;
-    if (c->source == 0 && whole(c)) {
+    if (c->source == 0) {
         FixedGraph* fg = nullptr;
-        if ((st = get_fixed_graph(c, steps, parity, dt, R, &fg))) return st;
+        if ((st = get_fixed_graph(c, B, steps, parity, dt, R, &fg))) return st;
         CK(cudaGraphLaunch(fg->exec, c->stream));
-        if (kernels)
-            *kernels += (gauges ? steps : 0) + (c->fused == 2   ? steps
-                                                : c->fused == 3 ? 2 * steps
-                                                : c->fused == 1 ? 2 * steps + 1
-                                                                : 3 * steps);
-    } else if (c->source == 0 && c->fused == 3 && !gauges) {
-        // slab context: the fused structure with NCCL halo exchanges between
-        // the kernels (direct launches)
-        reset_recs(c, steps);
-        if ((st = enqueue_chunk_s12(c, parity, steps, dt, nullptr))) return st;
-        if (kernels) *kernels += 2 * steps;
-    } else {
-        hsgn_state* Y[2] = {&c->ws[0], &c->ws[1]};
-        hsgn_state* K[2] = {&c->ws[2], &c->ws[3]};
-        reset_recs(c, steps);
-        double ts = t;
-        for (int s = 0; s < steps; ++s) {
-            const int p = (parity + s) & 1;
-            st = enqueue_step(c, Y[p], K[p], &c->ws[4], Y[p ^ 1], K[p ^ 1], nullptr, &c->d_rec[s],
-                              s ? &c->d_rec[s - 1] : nullptr, ts, dt, false, 0, 0, kernels);
-            if (st) return st;
-            if (gauges) {
-                CK(launch_gauges(Y[p ^ 1]->base, c->b, R->d_idx, (int)R->gi.size(),
-                                 R->d_gauge + (size_t)s * R->gi.size(), c->stream));
-                if (kernels) ++*kernels;
-            }
-            ts = ts + dt;
-        }
+        c->launches += fg->kernels;
+    } else if ((st = enqueue_chunk(c, B, parity, steps, t, dt, R))) {
+        return st;
     }
     CK(cudaMemcpyAsync(c->h_rec, c->d_rec, sizeof(StepRec) * steps, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
+    if (c->ktiming && whole(c) && c->fused == 3 && c->source == 0) {  // the chunk's event nodes have fired
+        for (int s = 0; s < steps; ++s) {
+            float a = 0.f, b = 0.f;
+            CK(cudaEventElapsedTime(&a, c->kev[3 * s], c->kev[3 * s + 1]));
+            CK(cudaEventElapsedTime(&b, c->kev[3 * s + 2], c->kev[3 * s + 3]));
+            c->kt_ms[0] += a;
+            c->kt_ms[1] += b;
+        }
+        c->kt_n += steps;
+    }
     *done = steps;
     *fail_kind = 0;
     for (int s = 0; s < steps; ++s) {
@@ -1257,6 +1268,7 @@ static hsgn_status wrms(hsgn_ctx* c, const hsgn_state* x, const hsgn_state* ref,
     const long long n = (long long)c->ny_loc * c->grid.nx;
     CK(launch_wrms(x->base, ref->base, atol, rtol, n, c->fs, c->d_err_part, c->stream));
     CK(launch_sum_partials(c->d_err_part, wrms_blocks(), c->d_scalar, c->stream));
+    c->launches += 2;
     hsgn_status st = agree(c, c->d_scalar, 1, NCCL_FLOAT64, NCCL_SUM);
     if (st) return st;
     double s = 0;
@@ -1301,6 +1313,7 @@ static hsgn_status rec_gauges_now(hsgn_recorder* R, double t, const hsgn_state* 
     hsgn_ctx* c = R->c;
     if (R->gi.empty()) return HSGN_OK;
     CK(launch_gauges(q->base, c->b, R->d_idx, (int)R->gi.size(), R->d_gauge, c->stream));
+    ++c->launches;
     return rec_collect_gauges(R, &t, 1);
 }
 
@@ -1340,6 +1353,7 @@ static hsgn_status rec_accept(hsgn_recorder* R, double t, const hsgn_state* q, c
     if (R->accept_count % R->stride == 0) {
         const int ny = c->ny_loc;
         CK(launch_cons_rows(c->aux, q->base, qt->base, R->d_cons, c->stream));
+        ++c->launches;
         CK(cudaMemcpyAsync(R->h_cons, R->d_cons, sizeof(double) * 3 * ny, cudaMemcpyDeviceToHost, c->stream));
         CK(cudaStreamSynchronize(c->stream));
         R->cons.push_back(t);
@@ -1364,6 +1378,7 @@ extern "C" hsgn_status hsgn_solve_recorded(hsgn_ctx* c, const hsgn_state* q0, do
     rec->t = t0;
     hsgn_status st;
     const int CHUNK = 64;
+    const int64_t l0 = c->launches;
     if ((st = ensure_ws(c, CHUNK))) return st;
     c->base.h_floor = cfg->h_floor;  // the stage kernels' halt test and the chunk scan use the run's floor
     auto copy_state = [&](const hsgn_state* src, hsgn_state* dst) -> hsgn_status {
@@ -1371,21 +1386,27 @@ extern "C" hsgn_status hsgn_solve_recorded(hsgn_ctx* c, const hsgn_state* q0, do
                            cudaMemcpyDeviceToDevice, c->stream));
         return HSGN_OK;
     };
-    if ((st = copy_state(q0, q_out))) return st;
     if (!(t_final > t0)) {
+        if ((st = copy_state(q0, q_out))) return st;
         CK(cudaStreamSynchronize(c->stream));
         if (t_final == t0) return HSGN_OK;
         rec->aborted = 1;
         snprintf(rec->reason, sizeof rec->reason, "t_final precedes t0");
         return HSGN_OK;
     }
-    // buffers: y = ws[p], k1 = ws[2+p], k2 = ws[4], part = ws[5], scratch ws[6], ws[7]
+    // buffers: y = B.Y[p], k1 = B.K[p], k2 = ws[4], part = ws[5], scratch ws[6], ws[7].
+    // The caller's output state is the integrator's parity-0 y buffer (one
+    // copy of q0 in, none out after an even number of accepted steps).
+    Bufs B = ws_bufs(c);
+    if (q_out != q0) B.Y[0] = q_out;
     int p = 0;
-    if ((st = copy_state(q0, &c->ws[0]))) return st;
+    if ((st = copy_state(q0, B.Y[0]))) return st;
     double t = t0;
     auto abort_with = [&](const char* why) -> hsgn_status {
-        hsgn_status s2 = copy_state(&c->ws[p], q_out);
-        if (s2) return s2;
+        if (B.Y[p] != q_out) {
+            hsgn_status s2 = copy_state(B.Y[p], q_out);
+            if (s2) return s2;
+        }
         CK(cudaStreamSynchronize(c->stream));
         rec->t = t;
         rec->aborted = 1;
@@ -1393,7 +1414,7 @@ extern "C" hsgn_status hsgn_solve_recorded(hsgn_ctx* c, const hsgn_state* q0, do
         return HSGN_OK;
     };
     char why[256];
-    st = rhs_eval(c, t, &c->ws[0], &c->ws[2]);
+    st = rhs_eval(c, t, B.Y[0], B.K[0]);
     if (st == HSGN_EDEPTH) {
         snprintf(why, sizeof why, "initial tendency: %s", c->err.c_str());
         return abort_with(why);
@@ -1411,24 +1432,26 @@ extern "C" hsgn_status hsgn_solve_recorded(hsgn_ctx* c, const hsgn_state* q0, do
         // estimate_initial_dt (time_integration.hpp:170-203)
         const double dt_cap = smin(cfg->dt_max, t_final - t0);
         double d0, d1;
-        if ((st = wrms(c, &c->ws[0], &c->ws[0], cfg->abs_tol, cfg->rel_tol, &d0))) return st;
-        if ((st = wrms(c, &c->ws[2], &c->ws[0], cfg->abs_tol, cfg->rel_tol, &d1))) return st;
+        if ((st = wrms(c, B.Y[0], B.Y[0], cfg->abs_tol, cfg->rel_tol, &d0))) return st;
+        if ((st = wrms(c, B.K[0], B.Y[0], cfg->abs_tol, cfg->rel_tol, &d1))) return st;
         if (d1 == 0.0) {
             dt = dt_cap;
         } else {
             double h0 = (d0 >= 1e-5 && d1 >= 1e-5) ? 0.01 * d0 / d1 : 1e-6;
             h0 = smin(h0, dt_cap);
             const long long n = (long long)c->ny_loc * c->grid.nx;
-            CK(launch_axpy5(c->ws[0].base, h0, c->ws[2].base, c->ws[6].base, n, c->fs, c->stream));
+            CK(launch_axpy5(B.Y[0]->base, h0, B.K[0]->base, c->ws[6].base, n, c->fs, c->stream));
+            ++c->launches;
             if ((st = exchange(c, &c->ws[6], 5))) return st;
             double d2 = 0.0;
             bool probed = false;
             st = rhs_eval(c, t0 + h0, &c->ws[6], &c->ws[7]);
             if (st == HSGN_OK) {
                 ++rec->rhs_evals_setup;
-                CK(launch_axpy5(c->ws[7].base, -1.0, c->ws[2].base, c->ws[6].base, n, c->fs, c->stream));
+                CK(launch_axpy5(c->ws[7].base, -1.0, B.K[0]->base, c->ws[6].base, n, c->fs, c->stream));
+                ++c->launches;
                 double r;
-                if ((st = wrms(c, &c->ws[6], &c->ws[0], cfg->abs_tol, cfg->rel_tol, &r))) return st;
+                if ((st = wrms(c, &c->ws[6], B.Y[0], cfg->abs_tol, cfg->rel_tol, &r))) return st;
                 d2 = r / h0;
                 probed = true;
             } else if (st != HSGN_EDEPTH) {
@@ -1448,18 +1471,17 @@ extern "C" hsgn_status hsgn_solve_recorded(hsgn_ctx* c, const hsgn_state* q0, do
         rec->rhs_evals += rec->rhs_evals_setup;
     }
     if (R) {
-        if ((st = rec_gauges_now(R, t, &c->ws[0]))) return st;
-        if ((st = rec_accept(R, t, &c->ws[0], &c->ws[2], nullptr))) return st;
+        if ((st = rec_gauges_now(R, t, B.Y[0]))) return st;
+        if ((st = rec_accept(R, t, B.Y[0], B.K[0], nullptr))) return st;
     }
     if (obs) {
         CK(cudaStreamSynchronize(c->stream));
-        obs(t, &c->ws[0], &c->ws[2], user);
+        obs(t, B.Y[0], B.K[0], user);
     }
 
     const double order_exp = 1.0 / 3.0;
     double err_prev = 1.0;
     const double tiny = 4.0 * std::numeric_limits<double>::epsilon();
-    int64_t kernels = 0;
 
     while (t < t_final - tiny * smax(1.0, std::fabs(t_final))) {
         if (rec->accepted + rec->rejected >= cfg->max_steps) {
@@ -1495,7 +1517,7 @@ extern "C" hsgn_status hsgn_solve_recorded(hsgn_ctx* c, const hsgn_state* q0, do
             if (n >= 2) {
                 if ((n & 1) && !R) --n;  // even chunks keep the buffer parity (fewer graphs)
                 int done = 0, fk = 0, fs_ = 0;
-                if ((st = run_fixed_chunk(c, p, n, t, dt, &done, &fk, &fs_, &kernels, R))) return st;
+                if ((st = run_fixed_chunk(c, B, p, n, t, dt, &done, &fk, &fs_, R))) return st;
                 for (int s = 0; s < done; ++s) {
                     t = t + dt;
                     ++rec->accepted;
@@ -1508,7 +1530,7 @@ extern "C" hsgn_status hsgn_solve_recorded(hsgn_ctx* c, const hsgn_state* q0, do
                     if (done == n) {  // steps 1..n-1 carry no record by construction
                         R->accept_count += n - 1;
                         R->prev_t = ts[n - 2];
-                        if ((st = rec_accept(R, t, &c->ws[p], &c->ws[2 + p], &c->ws[p ^ 1]))) return st;
+                        if ((st = rec_accept(R, t, B.Y[p], B.K[p], B.Y[p ^ 1]))) return st;
                     } else {
                         R->accept_count += done;
                     }
@@ -1533,22 +1555,21 @@ extern "C" hsgn_status hsgn_solve_recorded(hsgn_ctx* c, const hsgn_state* q0, do
         const int q = p ^ 1;
         reset_recs(c, 1);
         if (c->fused == 3 && c->source == 0) {  // S12 + S3 (with error partials when adaptive)
-            st = enqueue_s12(c, &c->ws[p], &c->ws[2 + p], &c->ws[q], &c->d_rec[0], nullptr, dt,
-                             fixed ? nullptr : &c->ws[5]);
-            if (!st) st = exchange(c, &c->ws[q], 5);
+            st = enqueue_s12(c, B.Y[p], B.K[p], B.Y[q], &c->d_rec[0], nullptr, dt, fixed ? nullptr : &c->ws[5]);
+            if (!st) st = exchange(c, B.Y[q], 5);
             if (!st)
-                st = enqueue_stage(c, 3, &c->ws[p], &c->ws[2 + p], &c->ws[4], &c->ws[q], &c->ws[2 + q], &c->ws[5],
-                                   &c->d_rec[0], nullptr, t, dt, !fixed, cfg->abs_tol, cfg->rel_tol);
-            if (!st) st = exchange(c, &c->ws[2 + q], 5);
+                st = enqueue_stage(c, 3, B.Y[p], B.K[p], &c->ws[4], B.Y[q], B.K[q], &c->ws[5], &c->d_rec[0], nullptr, t,
+                                   dt, !fixed, cfg->abs_tol, cfg->rel_tol);
+            if (!st) st = exchange(c, B.K[q], 5);
             if (!st) st = agree_rec(c, &c->d_rec[0]);
-            kernels += 2;
         } else {
-            st = enqueue_step(c, &c->ws[p], &c->ws[2 + p], &c->ws[4], &c->ws[q], &c->ws[2 + q], &c->ws[5],
-                              &c->d_rec[0], nullptr, t, dt, !fixed, cfg->abs_tol, cfg->rel_tol, &kernels);
+            st = enqueue_step(c, B.Y[p], B.K[p], &c->ws[4], B.Y[q], B.K[q], &c->ws[5], &c->d_rec[0], nullptr, t, dt,
+                              !fixed, cfg->abs_tol, cfg->rel_tol);
         }
         if (st) return st;
         if (!fixed) {
             CK(launch_sum_partials(c->d_err_part, stage_grid_blocks(c->base), c->d_scalar, c->stream));
+            ++c->launches;
             if ((st = agree(c, c->d_scalar, 1, NCCL_FLOAT64, NCCL_SUM))) return st;
         }
         StepRec r;
@@ -1598,20 +1619,20 @@ extern "C" hsgn_status hsgn_solve_recorded(hsgn_ctx* c, const hsgn_state* q0, do
                 err_prev = smax(err, 1e-10);
             }
             if (R) {
-                if ((st = rec_gauges_now(R, t, &c->ws[p]))) return st;
-                if ((st = rec_accept(R, t, &c->ws[p], &c->ws[2 + p], &c->ws[p ^ 1]))) return st;
+                if ((st = rec_gauges_now(R, t, B.Y[p]))) return st;
+                if ((st = rec_accept(R, t, B.Y[p], B.K[p], B.Y[p ^ 1]))) return st;
             }
-            if (obs) obs(t, &c->ws[p], &c->ws[2 + p], user);
+            if (obs) obs(t, B.Y[p], B.K[p], user);
         } else {
             ++rec->rejected;
             const double fac = std::isfinite(err) ? sclamp(cfg->safety * std::pow(err, -order_exp), 0.1, 0.9) : 0.1;
             dt *= fac;
         }
     }
-    if ((st = copy_state(&c->ws[p], q_out))) return st;
+    if (B.Y[p] != q_out && (st = copy_state(B.Y[p], q_out))) return st;
     CK(cudaStreamSynchronize(c->stream));
     rec->t = t;
-    c->last_kernels = kernels;
+    c->last_kernels = c->launches - l0;
     return HSGN_OK;
 }
 
@@ -1626,7 +1647,9 @@ extern "C" hsgn_status hsgn_recorder_create(hsgn_ctx* c, int32_t n_gauges, const
     if (!whole(c)) return fail(c, HSGN_EINVAL, "the recorder needs a whole-grid context");
     DeviceGuard dg_(c->device);
     hsgn_recorder* R = new hsgn_recorder;
+    static uint64_t next_id = 0;
     R->c = c;
+    R->id = ++next_id;
     R->stride = conservation_stride;
     const hsgn_grid& g = c->grid;
     std::vector<long long> idx;
@@ -1665,7 +1688,18 @@ extern "C" hsgn_status hsgn_recorder_destroy(hsgn_recorder* R) {
     if (!R) return HSGN_OK;
     DeviceRestore dr_;
     if (R->c) cudaSetDevice(R->c->device);
-    if (R->c) cudaStreamSynchronize(R->c->stream);  // pending snapshot copies
+    if (R->c) {
+        cudaStreamSynchronize(R->c->stream);  // pending snapshot copies
+        // the gauge-sampling graphs captured this recorder's buffers
+        for (auto it = R->c->graphs.begin(); it != R->c->graphs.end();) {
+            if (std::get<2>(it->first) == R->id) {
+                cudaGraphExecDestroy(it->second.exec);
+                it = R->c->graphs.erase(it);
+            } else {
+                ++it;
+            }
+        }
+    }
     cudaFree(R->d_idx);
     cudaFree(R->d_gauge);
     cudaFreeHost(R->h_gauge);
@@ -1723,20 +1757,30 @@ extern "C" hsgn_status hsgn_recorder_snapshot(const hsgn_recorder* R, int32_t k,
     return HSGN_OK;
 }
 
-extern "C" hsgn_status hsgn_prepare_fixed_steps(hsgn_ctx* c, double dt, int64_t steps) {
-    if (!c || steps < 0) return HSGN_EINVAL;
+// The buffers of hsgn_bs3_fixed_steps: the caller's (y, k1) are parity 0,
+// the workspace pair parity 1, so an even number of steps ends in place.
+static Bufs caller_bufs(hsgn_ctx* c, hsgn_state* y, hsgn_state* k1) {
+    return Bufs{{y, &c->ws[1]}, {k1, &c->ws[3]}};
+}
+
+static const int FIXED_CHUNK = 64;  // steps per captured graph of hsgn_bs3_fixed_steps
+
+extern "C" hsgn_status hsgn_prepare_fixed_steps(hsgn_ctx* c, hsgn_state* y, hsgn_state* k1, double dt,
+                                                int64_t steps) {
+    if (!c || !y || !k1 || steps < 0) return HSGN_EINVAL;
     DeviceGuard dg_(c->device);
-    const int CHUNK = 64;  // the chunking of hsgn_bs3_fixed_steps (even chunks keep buffer parity 0)
     hsgn_status st;
-    if ((st = ensure_ws(c, CHUNK))) return st;
-    if (!whole(c) || c->source) return HSGN_OK;  // direct launches: nothing to build
+    if ((st = ensure_ws(c, FIXED_CHUNK))) return st;
+    if (c->source) return HSGN_OK;  // direct launches: nothing to build
     c->base.h_floor = c->phys.h_floor;
-    for (int64_t left = steps; left > 1;) {
-        int n = (int)std::min<int64_t>(CHUNK, left);
-        if (n & 1) --n;
+    const Bufs B = caller_bufs(c, y, k1);
+    int p = 0;
+    for (int64_t left = steps; left > 0;) {  // the chunk sequence of hsgn_bs3_fixed_steps
+        const int n = (int)std::min<int64_t>(FIXED_CHUNK, left);
         FixedGraph* fg = nullptr;
-        if ((st = get_fixed_graph(c, n, 0, dt, nullptr, &fg))) return st;
+        if ((st = get_fixed_graph(c, B, n, p, dt, nullptr, &fg))) return st;
         left -= n;
+        p ^= n & 1;
     }
     return HSGN_OK;
 }
@@ -1746,38 +1790,22 @@ extern "C" hsgn_status hsgn_bs3_fixed_steps(hsgn_ctx* c, hsgn_state* y, hsgn_sta
     if (!c || !y || !k1 || steps < 0) return HSGN_EINVAL;
     DeviceGuard dg_(c->device);
     hsgn_status st;
-    const int CHUNK = 64;
-    if ((st = ensure_ws(c, CHUNK))) return st;
+    if ((st = ensure_ws(c, FIXED_CHUNK))) return st;
     c->base.h_floor = c->phys.h_floor;
-    // y, k1 are caller buffers: run in the workspace pair and copy back
-    CK(cudaMemcpyAsync(c->ws[0].base - GHOST * c->grid.nx, y->base - GHOST * c->grid.nx, sizeof(double) * 5 * c->fs,
-                       cudaMemcpyDeviceToDevice, c->stream));
-    CK(cudaMemcpyAsync(c->ws[2].base - GHOST * c->grid.nx, k1->base - GHOST * c->grid.nx, sizeof(double) * 5 * c->fs,
-                       cudaMemcpyDeviceToDevice, c->stream));
+    // in place on the caller's buffers (workspace pair for odd steps); the
+    // event window covers everything the call does on the device
+    const Bufs B = caller_bufs(c, y, k1);
     int p = 0;
-    int64_t done_total = 0, kernels = 0;
+    int64_t done_total = 0;
+    const int64_t l0 = c->launches;
+    c->kt_ms[0] = c->kt_ms[1] = 0.0;
+    c->kt_n = 0;
     CK(cudaEventRecord(c->ev0, c->stream));
     hsgn_status result = HSGN_OK;
     while (done_total < steps) {
-        int n = (int)std::min<int64_t>(CHUNK, steps - done_total);
+        const int n = (int)std::min<int64_t>(FIXED_CHUNK, steps - done_total);
         int done = 0, fk = 0, fs_ = 0;
-        if (n == 1) {
-            // single odd step: direct launches
-            hsgn_state* Y[2] = {&c->ws[0], &c->ws[1]};
-            hsgn_state* K[2] = {&c->ws[2], &c->ws[3]};
-            reset_recs(c, 1);
-            if ((st = enqueue_step(c, Y[p], K[p], &c->ws[4], Y[p ^ 1], K[p ^ 1], nullptr, &c->d_rec[0], nullptr, t,
-                                   dt, false, 0, 0, &kernels)))
-                return st;
-            StepRec r;
-            CK(cudaMemcpyAsync(&r, &c->d_rec[0], sizeof r, cudaMemcpyDeviceToHost, c->stream));
-            CK(cudaStreamSynchronize(c->stream));
-            done = (r.bad[0] | r.bad[1] | r.bad[2]) ? 0 : 1;
-            fk = done ? 0 : 1;
-        } else {
-            if (n & 1) --n;
-            if ((st = run_fixed_chunk(c, p, n, t, dt, &done, &fk, &fs_, &kernels))) return st;
-        }
+        if ((st = run_fixed_chunk(c, B, p, n, t, dt, &done, &fk, &fs_))) return st;
         for (int s = 0; s < done; ++s) {
             t = t + dt;
             p ^= 1;
@@ -1794,18 +1822,35 @@ extern "C" hsgn_status hsgn_bs3_fixed_steps(hsgn_ctx* c, hsgn_state* y, hsgn_sta
             break;
         }
     }
+    if (p) {  // odd number of completed steps: the last state is in the workspace pair
+        CK(cudaMemcpyAsync(y->base - GHOST * c->grid.nx, B.Y[1]->base - GHOST * c->grid.nx,
+                           sizeof(double) * 5 * c->fs, cudaMemcpyDeviceToDevice, c->stream));
+        CK(cudaMemcpyAsync(k1->base - GHOST * c->grid.nx, B.K[1]->base - GHOST * c->grid.nx,
+                           sizeof(double) * 5 * c->fs, cudaMemcpyDeviceToDevice, c->stream));
+    }
     CK(cudaEventRecord(c->ev1, c->stream));
-    CK(cudaMemcpyAsync(y->base - GHOST * c->grid.nx, c->ws[p].base - GHOST * c->grid.nx, sizeof(double) * 5 * c->fs,
-                       cudaMemcpyDeviceToDevice, c->stream));
-    CK(cudaMemcpyAsync(k1->base - GHOST * c->grid.nx, c->ws[2 + p].base - GHOST * c->grid.nx, sizeof(double) * 5 * c->fs,
-                       cudaMemcpyDeviceToDevice, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     float ms = 0.f;
     cudaEventElapsedTime(&ms, c->ev0, c->ev1);
     c->last_ms = ms;
-    c->last_kernels = kernels;
+    c->last_kernels = c->launches - l0;
     if (steps_done) *steps_done = done_total;
     return result;
+}
+
+extern "C" hsgn_status hsgn_set_kernel_timing(hsgn_ctx* c, int32_t on) {
+    if (!c) return HSGN_EINVAL;
+    c->ktiming = on ? 1 : 0;
+    return HSGN_OK;
+}
+
+extern "C" hsgn_status hsgn_kernel_times(const hsgn_ctx* c, double* s12_ms, double* s3_ms, int64_t* steps) {
+    if (!c) return HSGN_EINVAL;
+    const double n = c->kt_n ? (double)c->kt_n : 1.0;
+    if (s12_ms) *s12_ms = c->kt_ms[0] / n;
+    if (s3_ms) *s3_ms = c->kt_ms[1] / n;
+    if (steps) *steps = c->kt_n;
+    return HSGN_OK;
 }
 
 // Per-stage device time of the fused step (CUDA events around each stage
@@ -1870,13 +1915,11 @@ extern "C" hsgn_status hsgn_profile_stages(hsgn_ctx* c, const hsgn_state* y, con
     return HSGN_OK;
 }
 
-// Mean device ms of the fused S3+S1 kernel (S31) over `reps` launches on the
-// ynew of one step from (y, k1) (workspace copies; caller state intact).
+// Mean device ms of the fused S12 kernel (stages 1 + 2) over `reps` launches
+// on workspace copies of (y, k1) (caller state intact).
 extern "C" hsgn_status hsgn_profile_fused(hsgn_ctx* c, const hsgn_state* y, const hsgn_state* k1, double dt,
                                           int32_t reps, double* ms) {
     if (!c || !y || !k1 || !ms || reps < 1) return HSGN_EINVAL;
-    if (!whole(c) && c->fused != 3)  // slabs run S12 + S3 (or the per-stage kernels)
-        return fail(c, HSGN_EINVAL, "the S31 / whole-step kernels need a whole-grid context");
     DeviceGuard dg_(c->device);
     hsgn_status st;
     if ((st = ensure_ws(c, 2))) return st;
@@ -1885,36 +1928,13 @@ extern "C" hsgn_status hsgn_profile_fused(hsgn_ctx* c, const hsgn_state* y, cons
     CK(cudaMemcpyAsync(c->ws[2].base - GHOST * c->grid.nx, k1->base - GHOST * c->grid.nx, sizeof(double) * 5 * c->fs,
                        cudaMemcpyDeviceToDevice, c->stream));
     reset_recs(c, 2);
-    for (int stage = 1; stage <= 2; ++stage)
-        if ((st = enqueue_stage(c, stage, &c->ws[0], &c->ws[2], &c->ws[4], &c->ws[1], &c->ws[3], nullptr,
-                                &c->d_rec[0], nullptr, 0.0, dt, false, 0, 0)))
-            return st;
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
     double acc = 0.0;
     for (int r = 0; r < reps; ++r) {
         CK(cudaEventRecord(e0, c->stream));
-        if (c->fused == 3) {
-            StageArgs A = stage_args(c, MODE_S12, 0.0);
-            A.a = 0.5 * dt;
-            A.a2 = 0.75 * dt;
-            A.c1 = dt * (2.0 / 9.0);
-            A.c2 = dt * (1.0 / 3.0);
-            A.c3 = dt * (4.0 / 9.0);
-            A.y = c->ws[0].base;
-            A.k = c->ws[2].base;
-            A.out = c->ws[6].base;
-            A.bad = &c->d_rec[1].bad[0];
-            A.bad2 = &c->d_rec[1].bad[1];
-            A.minh = &c->d_rec[1].minh;
-            st = launch(c, MODE_S12, A);
-        } else if (c->fused == 2)
-            st = enqueue_step_kernel(c, &c->ws[0], &c->ws[2], &c->ws[6], &c->ws[7], &c->d_rec[1], nullptr, dt);
-        else
-            st = enqueue_stage(c, 31, &c->ws[0], &c->ws[2], &c->ws[4], &c->ws[1], &c->ws[3], nullptr, &c->d_rec[1],
-                               &c->d_rec[0], 0.0, dt, false, 0, 0);
-        if (st) return st;
+        if ((st = enqueue_s12(c, &c->ws[0], &c->ws[2], &c->ws[6], &c->d_rec[1], nullptr, dt))) return st;
         CK(cudaEventRecord(e1, c->stream));
         CK(cudaEventSynchronize(e1));
         float m = 0.f;

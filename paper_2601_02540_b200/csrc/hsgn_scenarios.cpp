@@ -461,14 +461,20 @@ hsgn_status hsgn_scenario_make(const char* name, const char* const* keys, const 
 }
 
 hsgn_status hsgn_scenario_sample(const hsgn_scenario* s, int32_t nx, int32_t ny, double* b, double* q) {
-    if (!s || !b || !q || s->kind < 0 || s->kind >= NKIND || nx < 4 || ny < 4) return HSGN_EINVAL;
-    const size_t n = (size_t)nx * (size_t)ny;
+    return hsgn_scenario_sample_rows(s, nx, ny, 0, ny, b, q);
+}
+
+hsgn_status hsgn_scenario_sample_rows(const hsgn_scenario* s, int32_t nx, int32_t ny, int32_t j0, int32_t j1,
+                                      double* b, double* q) {
+    if (!s || !b || !q || s->kind < 0 || s->kind >= NKIND || nx < 4 || ny < 4 || j0 < 0 || j1 > ny || j1 <= j0)
+        return HSGN_EINVAL;
+    const size_t n = (size_t)nx * (size_t)(j1 - j0);
     std::vector<double> xs(nx);
     for (int i = 0; i < nx; ++i) xs[i] = node_x(s, nx, i);
-    for (int j = 0; j < ny; ++j) {
+    for (int j = j0; j < j1; ++j) {
         const double y = node_y(s, ny, j);
         for (int i = 0; i < nx; ++i) {
-            const size_t k = (size_t)j * nx + i;
+            const size_t k = (size_t)(j - j0) * nx + i;
             initial(s, xs[i], y, &b[k], &q[k], &q[n + k], &q[2 * n + k]);
             q[3 * n + k] = 0.0;  // w, eta: init_auxiliary (model.hpp:93-105)
             q[4 * n + k] = 0.0;

@@ -90,6 +90,20 @@ def sample_initial(spec: ScenarioSpec, nx: int, ny: int) -> Tuple[np.ndarray, np
     return b, q
 
 
+def sample_rows(spec: ScenarioSpec, nx: int, ny: int, j0: int, j1: int) -> Tuple[np.ndarray, np.ndarray]:
+    """sample_initial restricted to global rows [j0, j1) (a slab): b
+    ((j1-j0)*nx), q (5*(j1-j0)*nx) with w = eta = 0."""
+    spec.grid(nx, ny)
+    m = (j1 - j0) * nx
+    b = np.empty(m)
+    q = np.empty(5 * m)
+    st = N.lib().hsgn_scenario_sample_rows(C.byref(spec._c), nx, ny, j0, j1, b.ctypes.data_as(N.PD),
+                                           q.ctypes.data_as(N.PD))
+    if st:
+        raise ValueError(f"hsgn_scenario_sample_rows failed ({st})")
+    return b, q
+
+
 def evaluate(spec: ScenarioSpec, x: float, y: float):
     """The spec's closed forms at one point: (b, h0, u0, v0)(x, y)
     (spec.bathymetry / h0 / u0 / v0, scenarios.hpp:31-34)."""
@@ -143,5 +157,6 @@ def study_case(spec: ScenarioSpec, nx: int, ny: int, device: int = -1) -> Prepar
     return prepare_run(spec, nx, ny, device)
 
 
-__all__ = ["ScenarioSpec", "PreparedRun", "scenario_names", "make_scenario", "sample_initial", "exact_state", "evaluate",
+__all__ = ["ScenarioSpec", "PreparedRun", "scenario_names", "make_scenario", "sample_initial", "sample_rows",
+           "exact_state", "evaluate",
            "prepare_run", "study_case", "FIELD_NAMES"]

@@ -56,3 +56,29 @@ def benchmark_case(n: int = 8192):
     """Config 4 of BASELINE.json: (grid, q0, b, lambda, dt)."""
     g, q, b = mms_fields(n, n, 0.3)
     return g, q, b, 500.0, 0.25 * g.dx / 20.0
+
+
+def bench_case(bc: str, nx: int, ny: int, rows=None):
+    """The benchmark workloads (BASELINE configs 4 and 5) on an nx x ny grid,
+    optionally only global rows (j0, j1) of it (a slab's share).
+
+    * ``periodic``: the config-4 input -- manufactured bathymetry and state at
+      t = 0.3 -- on [-1, 1] x [-1, -1 + 2 ny / nx] (dx == dy, so every nx with
+      nx | 2^k keeps the common-factor stencil; the state has period 1 in y,
+      so a 2P-long domain is the same smooth periodic input);
+    * ``reflecting``: ``gaussian_obstacle(bounded)`` (scenarios.hpp:356-383) --
+      walls on all four sides, SBP closures and SAT -- sampled by the
+      scenario library; w and eta come from the device init_auxiliary
+      (``needs_aux``).
+    Returns (grid, q, b, lambda, dt, needs_aux)."""
+    if bc == "periodic":
+        g, q, b = mms_fields(nx, ny, 0.3, y_max=-1.0 + 2.0 * ny / nx, rows=rows)
+        return g, q, b, 500.0, 0.25 * g.dx / 20.0, False
+    if bc == "reflecting":
+        from .scenarios import make_scenario, sample_rows
+        spec = make_scenario("gaussian_obstacle", {"bounded": 1.0})
+        g = spec.grid(nx, ny)
+        j0, j1 = rows if rows is not None else (0, ny)
+        b, q = sample_rows(spec, nx, ny, j0, j1)
+        return g, q, b, spec.lambda_, 0.25 * min(g.dx, g.dy) / 20.0, True
+    raise ValueError(f"unknown boundary workload {bc!r}")

@@ -1,10 +1,11 @@
-"""GPU: the fused stage-3 + next-stage-1 kernel (S31).
+"""GPU: the fused stage-1 + stage-2 kernel (S12).
 
-The fixed-step graphs of a whole-grid context run S1, S2, (S31, S2)...,
-S3.  S31 must reproduce the unfused S3 and S1 bit for bit, including at
-the tile seams (124 finished columns per CTA, two halo columns each side),
-the CTA row seams (the S3 half re-runs one row above and below each strip)
-and the wrap / clamp rows, and it must keep the reference's failure
+The fixed-step graphs run S12 + S3 per step (mode 3, the default) or one
+kernel per stage (mode 0).  S12 must reproduce the unfused S1 and S2 bit
+for bit, including at the tile seams (124 finished columns per CTA, two
+halo columns each side), the CTA row seams (stage 1 re-runs one row above
+and below each strip), the wrap / clamp rows and the edge / interior tile
+split of grids with walls, and it must keep the reference's failure
 semantics (which stage of which step failed, the abort reason, the ledger
 and the last valid state).
 """
@@ -48,7 +49,7 @@ def test_fused_fixed_steps_bitwise(orc, nx, ny, kx, ky, rpb):
     g, ctx = _ctx(og, b)
     if rpb:
         ctx.set_rows_per_block(rpb)
-    for mode in (0, 1, 2, 3):
+    for mode in (0, 3):
         ctx.fused_stages = mode
         assert ctx.fused_stages == mode
         res = H.adaptive_solve(ctx, H.StateField(g, q), 0.0, T, H.IntegratorConfig(fixed_dt=dt))
@@ -65,12 +66,12 @@ def _drying_state(nx, ny, amp, U):
     return np.concatenate([h.ravel(), (U * X * e).ravel(), (U * Y * e).ravel(), np.zeros(nx * ny), h.ravel()])
 
 
-# (amp, U, dt, h_floor): failures at stage 1, at stage 3 (the S3 half of an
-# S31 launch), at the depth floor, and a floor hit on the first step
+# (amp, U, dt, h_floor): failures at stage 1, at stage 3, at the depth
+# floor, and a floor hit on the first step
 @pytest.mark.parametrize("amp,U,dt,floor", [(0.99, 10.0, 1e-3, 1e-12), (0.99, 30.0, 1e-3, 1e-12),
                                              (0.99, 10.0, 1e-3, 0.005), (0.999, 10.0, 1e-3, 0.005),
                                              (0.99, 10.0, 3e-3, 1e-12)])
-@pytest.mark.parametrize("fused", [0, 1, 2, 3])
+@pytest.mark.parametrize("fused", [0, 3])
 def test_fixed_step_failures_match_reference(orc, amp, U, dt, floor, fused):
     nx, ny = 64, 48
     og = omake_grid(nx, ny)
@@ -90,8 +91,8 @@ def test_fixed_step_failures_match_reference(orc, amp, U, dt, floor, fused):
 
 
 def test_fused_launch_count_and_profile():
-    """Kernels per n-step graph chunk: 3n per stage, 2n+1 with S31 (S1, S2,
-    (S31, S2)^(n-1), S3), n with the whole-step kernel."""
+    """Kernels per n-step graph chunk of a periodic grid: 3n per stage, 2n
+    with S12 + S3; the other structures are rejected."""
     nx = ny = 256
     og = omake_grid(nx, ny)
     q, b = mms_exact_field(og, 0.3)
@@ -99,10 +100,13 @@ def test_fused_launch_count_and_profile():
     y = ctx.state(H.StateField(g, q))
     k1 = ctx.state()
     H.rhs(ctx, 0.0, y, k1)
-    for mode, want in ((1, 2 * 64 + 1), (0, 3 * 64), (2, 64), (3, 2 * 64)):
+    for mode, want in ((0, 3 * 64), (3, 2 * 64)):
         ctx.fused_stages = mode
         done, ms, kernels = H.bs3_fixed_steps(ctx, y, k1, 0.0, 1e-5, 64)
         assert done == 64 and kernels == want, mode
+    for bad in (1, 2, 4):
+        with pytest.raises(ValueError):
+            ctx.fused_stages = bad
 
 
 @pytest.mark.parametrize("kind", [0, 1])
@@ -119,7 +123,7 @@ def test_fused_structures_deterministic_under_repetition(kind):
     dt = 0.25 * dx / 20.0
     first = None
     for rep in range(12):
-        for mode in (0, 1, 2, 3):
+        for mode in (0, 3):
             ctx.fused_stages = mode
             res = H.adaptive_solve(ctx, H.StateField(g, q), 0.0, 6 * dt, H.IntegratorConfig(fixed_dt=dt))
             flat = res.q.flat().copy()
@@ -128,12 +132,12 @@ def test_fused_structures_deterministic_under_repetition(kind):
             assert _neq(flat, first) == 0, (rep, mode)
 
 
-@pytest.mark.parametrize("kind", [0, 1])
-def test_adaptive_attempts_fused_equal_unfused(kind):
+@pytest.mark.parametrize("kind,nx,ny", [(0, 96, 80), (1, 96, 80), (0, 400, 96), (1, 401, 131)])
+def test_adaptive_attempts_fused_equal_unfused(kind, nx, ny):
     """Adaptive attempts run S12 (with the error partials) + S3 in mode 3:
     the error norms, hence the step sequence and the state, must equal the
-    per-stage path bit for bit."""
-    nx, ny = 96, 80
+    per-stage path bit for bit (the larger grids split into edge and
+    interior launches, whose error partials share one array)."""
     og = omake_grid(nx, ny, kind_x=kind, kind_y=kind)
     q, b = mms_exact_field(og, 0.3)
     g, ctx = _ctx(og, b)

@@ -166,6 +166,50 @@ def _worker(rank, nranks, port, kind_y, steps, q_shared, result, schedule="stage
                 k1_e = ext2_state(k4)                                   # k4 halo (2 rows)
             y = y_e[:, lo2:lo2 + n_loc]
             steps_left = 0
+        elif schedule == "overlap":
+            # the overlapped slab schedule of hsgn_host.cu enqueue_slab_step:
+            # S12 on the two-row edge bands -> ynew halo exchange -> S12 on the
+            # interior band -> S3 on the edge bands -> k4 halo exchange -> S3 on
+            # the interior band.  Every band is evaluated from ONLY the rows it
+            # reads (2 beyond it for S12, 1 for S3), so the exchanges provably
+            # need nothing but the edge bands.
+            G = 2
+
+            def band(fn, reach, j_a, j_b, *arrs):
+                """Rows [j_a, j_b) of fn(sub-arrays of the extended arrays
+                holding slab rows [j_a - reach, j_b + reach), clipped at a wall)."""
+                a = max(lo2 + j_a - reach, 0)
+                e = min(lo2 + j_b + reach, arrs[0].shape[1])
+                out = fn(*[x[:, a:e] if x.ndim == 3 else x[a:e] for x in arrs])
+                return out[:, lo2 + j_a - a:lo2 + j_b - a]
+
+            def s12(ys, ks, bs):
+                k2 = rhs_rows(ys + (0.5 * dt) * ks, bs)
+                k3 = rhs_rows(ys + (0.75 * dt) * k2, bs)
+                return ys + (dt * (2.0 / 9.0)) * ks + (dt * (1.0 / 3.0)) * k2 + (dt * (4.0 / 9.0)) * k3
+
+            def s3(ys, bs):
+                return rhs_rows(ys, bs)
+
+            def exch_rows(lo_rows, hi_rows, interior):
+                """Assemble the slab from its bands and add the exchanged
+                ghost rows (two per interior side), as the comm stream does."""
+                full = np.concatenate([lo_rows, interior, hi_rows], axis=1)
+                return np.stack([ext2(full[f]) for f in range(5)])
+
+            y_e, k1_e = ext2_state(y), ext2_state(k1)
+            for _ in range(steps):
+                yn_lo = band(s12, 2, 0, G, y_e, k1_e, b2)
+                yn_hi = band(s12, 2, n_loc - G, n_loc, y_e, k1_e, b2)
+                # (the exchange below only reads yn_lo / yn_hi)
+                yn_in = band(s12, 2, G, n_loc - G, y_e, k1_e, b2)
+                yn_e = exch_rows(yn_lo, yn_hi, yn_in)
+                k4_lo = band(s3, 1, 0, G, yn_e, b2)
+                k4_hi = band(s3, 1, n_loc - G, n_loc, yn_e, b2)
+                k4_in = band(s3, 1, G, n_loc - G, yn_e, b2)
+                y_e, k1_e = yn_e, exch_rows(k4_lo, k4_hi, k4_in)
+            y = y_e[:, lo2:lo2 + n_loc]
+            steps_left = 0
         else:
             steps_left = steps
         for _ in range(steps_left):
@@ -208,12 +252,14 @@ def _oracle_lib_patch():
     Oracle._lib_rhs_dxdy = rhs_dxdy
 
 
-@pytest.mark.parametrize("schedule", ["stage", "s12"])
+@pytest.mark.parametrize("schedule", ["stage", "s12", "overlap"])
 @pytest.mark.parametrize("nranks,kind_y", [(2, 0), (3, 0), (2, 1), (3, 1)])
 def test_slab_bs3_bitwise_equals_single_domain(nranks, kind_y, schedule):
     """schedule "stage": one ghost row, halos after every stage (the
     per-stage kernels); "s12": two ghost rows, halos of ynew after S12 and
-    of k4 after S3 (the default fused structure)."""
+    of k4 after S3 (the default fused structure); "overlap": the same with
+    edge-band / interior-band launches, the exchanges reading only the edge
+    bands (the NCCL slab schedule, hsgn_host.cu enqueue_slab_step)."""
     import sys
     sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
     from oracle_lib import Oracle, Phys, default_cfg, make_grid as omake, mms_exact_field

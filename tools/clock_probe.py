@@ -15,7 +15,7 @@ def clocks():
     out = subprocess.run(["nvidia-smi","--query-gpu=clocks.sm,power.draw,clocks_throttle_reasons.active","--format=csv,noheader"],capture_output=True,text=True).stdout.strip()
     return out
 for steps in (50, 300):
-    H.prepare_fixed_steps(ctx, dt, steps); H.bs3_fixed_steps(ctx, y, k1, 0.0, dt, 4)
+    H.prepare_fixed_steps(ctx, y, k1, dt, steps); H.bs3_fixed_steps(ctx, y, k1, 0.0, dt, 4)
     res = []
     def samp():
         for _ in range(6): res.append(clocks()); time.sleep(0.1)
