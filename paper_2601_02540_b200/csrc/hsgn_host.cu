@@ -317,6 +317,14 @@ static hsgn_status setup_ctx(hsgn_ctx* c) {
     const bool cf = p2 && A.cpx == A.cpy && !A.x_bounded && A.y_lo != YE_CLAMP && A.y_hi != YE_CLAMP && !A.walls;
     A.pow2 = cf ? 2 : (p2 ? 1 : 0);
     if (c->forced_kind >= 0 && c->forced_kind < A.pow2) A.pow2 = c->forced_kind;
+    // magnitude guard of the fast association (sgn_device.cuh lit_node): the
+    // constants must be zero or in [2^-60, 2^60], else every row is literal
+    auto guard_ok = [](double x) { return x == 0.0 || (std::fabs(x) >= 0x1p-60 && std::fabs(x) <= 0x1p60); };
+    A.lit_all = !(guard_ok(c->phys.g) && guard_ok(c->phys.lambda) && guard_ok(A.cpx) && guard_ok(A.cpy) &&
+                  guard_ok(A.c1x) && guard_ok(A.c1y) && guard_ok(A.tdx) && guard_ok(A.tdy));
+#ifdef HSGN_FORCE_LIT
+    A.lit_all = 1;  // experiments: literal association everywhere
+#endif
     A.g = c->phys.g;
     A.lambda = c->phys.lambda;
     A.lam_half = c->phys.lambda / 2.0;

@@ -141,11 +141,14 @@ __device__ __forceinline__ void load_raw(const KPtrs& P, unsigned off, Raw& r) {
 
 // Pointwise products of rhs.hpp:99-109 at one node from the stage input q
 // (h, u, v, w, eta) and b: stores the ring pairs of the node (S already
-// offset by ring row and column), fills the y-quantities; returns h > 0.
+// offset by ring row and column), fills the y-quantities and the node's
+// magnitude-guard flag (lit_node); returns h > 0.
 template <bool STORE_RH = true>
-__device__ __forceinline__ bool products_q(const double q[5], double b, double2* S, YQ& Y, double* rh_out) {
+__device__ __forceinline__ bool products_q(const double q[5], double b, double2* S, YQ& Y, double* rh_out,
+                                           bool& lit) {
     const double h = q[0], u = q[1], v = q[2], w = q[3], e = q[4];
     const bool ok = h > 0.0;
+    lit = lit_node(q, b);
     const double rh = rcp_or_nan(h);
     bool slow = false;
     double r = div_fast(e, h, rh, slow);  // eta/h computed once (rhs.hpp:86-88)
@@ -177,12 +180,13 @@ __device__ __forceinline__ bool products_q(const double q[5], double b, double2*
 // time_integration.hpp:61-75) for S1/S2, q = y otherwise; S2 also stores
 // ((y + c1 k1) + c2 k2), the k3-free part of ynew (state_add3).
 template <int MODE, bool STORE_RH = true>
-__device__ __forceinline__ bool products(const StageArgs& A, const Raw& raw, double2* S, YQ& Y, double* rh_out = nullptr) {
+__device__ __forceinline__ bool products(const StageArgs& A, const Raw& raw, double2* S, YQ& Y, bool& lit,
+                                         double* rh_out = nullptr) {
     double q[5];
 #pragma unroll
     for (int f = 0; f < 5; ++f)
         q[f] = (MODE == MODE_S1 || MODE == MODE_S2) ? dadd(raw.y[f], dmul(A.a, raw.k[f])) : raw.y[f];
-    const bool ok = products_q<STORE_RH>(q, raw.b, S, Y, rh_out);
+    const bool ok = products_q<STORE_RH>(q, raw.b, S, Y, rh_out, lit);
     if (MODE == MODE_S2) {
         double yp[5];
 #pragma unroll
@@ -316,6 +320,8 @@ struct Thr {
     int jc0, jc1;       // rows that use the y closure coefficient (clamped walls)
     unsigned long long bad, my_min;
     double my_err;
+    bool any;           // fast pass: a stage input this thread formed failed the magnitude guard
+    int t0;             // split-barrier step index of this pass's prologue
 };
 
 // x-quantities of a neighbour column re-formed from its ring pairs, with the
@@ -376,10 +382,18 @@ __device__ __forceinline__ void neighbour_y(const double2* S, YQ& Y) {
 // IN: interior tile of a grid with walls -- no node of the tile is a
 // closure or SAT node, so the continuity sum adds the SAT field's zero
 // exactly as the reference does ((-s) + 0.0) without the face predicates.
-template <int KIND, bool SW, bool SRC, bool IN>
+// LIT: the literal association of rhs.hpp:147-210 (every 0.5 where the
+// reference has it, the stencil coefficient inside every derivative: KIND 2
+// runs as KIND 1, which is exact for every input).  The fast association
+// (LIT = false) factors 0.5 out of the split groups and, for KIND 2, the
+// common stencil factor out of each tendency; it is used only where the
+// magnitude guard (lit_node) proves it bit-identical.
+template <int KIND, bool SW, bool SRC, bool IN, bool LIT>
 __device__ __forceinline__ void tendency(const StageArgs& A, const double2* S, int tid, int sl, int sr, double cx,
                                          double cy, bool xl, bool xr, int i, int j, const YQ& ypr, const YQ& ynr,
                                          double rh, double o[5]) {
+    constexpr int KD = (LIT && KIND == 2) ? 1 : KIND;  // derivative form
+    constexpr bool CF = KD == 2;                       // common factor applied once per tendency
     const double2* Sc = S + tid;  // row j, own column
     // centre values of row j (products re-formed as in rhs.hpp:99-109)
     const double2 c0 = Sc[P_HU * BX], c1 = Sc[P_VW * BX], c2 = Sc[P_EB * BX], c3 = Sc[P_RHB * BX];
@@ -389,16 +403,16 @@ __device__ __forceinline__ void tendency(const StageArgs& A, const double2* S, i
     XQ L, R;
     neighbour_x(S + sl, L);
     neighbour_x(S + sr, R);
-#define DX(f) const double d##f##_x = sbp_d<KIND>(cx, L.f, R.f)
-#define DY(f) const double d##f##_y = sbp_d<KIND>(cy, ypr.f, ynr.f)
+#define DX(f) const double d##f##_x = sbp_d<KD>(cx, L.f, R.f)
+#define DY(f) const double d##f##_y = sbp_d<KD>(cy, ypr.f, ynr.f)
     DX(h); DX(u); DX(v); DX(w); DX(e); DX(b); DX(hhb); DX(u2); DX(hu); DX(huv); DX(e2h); DX(huw);
     DY(h); DY(u); DY(v); DY(w); DY(e); DY(b); DY(hhb); DY(v2); DY(hv); DY(huv); DY(e2h); DY(hvw);
 #undef DX
 #undef DY
     const double g = A.g;
-    // KIND 2: every tendency sum is linear in the (undivided) differences, so
-    // the stencil coefficient is applied once per tendency (exact: power of 2)
-    auto sc = [&](double x) { return KIND == 2 ? dmul(A.cpx, x) : x; };
+    // KIND 2 (fast): every tendency sum is linear in the (undivided)
+    // differences, so the stencil coefficient is applied once per tendency
+    auto sc = [&](double x) { return CF ? dmul(A.cpx, x) : x; };
     // s + 0.5*G as one rounding: 0.5*G is exact, so fma(0.5, G, s) == RN(s + RN(0.5 G))
     auto add_half = [](double s, double G) { return __fma_rn(0.5, G, s); };
     {  // continuity (rhs.hpp:156-157) + wall SAT (sbp.hpp:272-284)
@@ -423,31 +437,59 @@ __device__ __forceinline__ void tendency(const StageArgs& A, const double2* S, i
     const double lt_r = dmul(A.lam_third, r);
     const double omr = dsub(1.0, r);
     const double lh_omr = dmul(A.lam_half, omr);
-    const double uv = dmul(u, v);
+    // relaxation groups (rhs.hpp:172-174, 185-187), formed where they are added
+    auto g3 = [&](double d_h, double d_e, double d_e2h, double d_b) {
+        return dadd(dsub(dsub(dadd(dmul(ls_rr, d_h), dmul(A.lam_third, d_e)), dmul(lt_r, d_e)),
+                         dmul(A.lam_sixth, d_e2h)),
+                    dmul(lh_omr, d_b));
+    };
     double nu, nv, nw;  // division numerators (before the common factor in KIND 2)
-    {  // x-momentum (rhs.hpp:167-175), 0.5 factored out of the two split groups
-        double s = dsub(dmul(g, dhhb_x), dmul(ghb, dh_x));
-        s = add_half(s, dsub(dadd(dsub(dmul(h, du2_x), dmul(u2, dh_x)), dmul(u, dhu_x)), dmul(hu, du_x)));
-        s = add_half(s, dsub(dadd(dsub(dhuv_y, dmul(uv, dh_y)), dmul(hv, du_y)), dmul(hu, dv_y)));
-        s = dadd(s, dadd(dsub(dsub(dadd(dmul(ls_rr, dh_x), dmul(A.lam_third, de_x)), dmul(lt_r, de_x)),
-                              dmul(A.lam_sixth, de2h_x)),
-                         dmul(lh_omr, db_x)));
-        nu = -s;
-    }
-    {  // y-momentum (rhs.hpp:180-188)
-        double s = dsub(dmul(g, dhhb_y), dmul(ghb, dh_y));
-        s = add_half(s, dsub(dadd(dsub(dmul(h, dv2_y), dmul(v2, dh_y)), dmul(v, dhv_y)), dmul(hv, dv_y)));
-        s = add_half(s, dsub(dadd(dsub(dhuv_x, dmul(uv, dh_x)), dmul(hu, dv_x)), dmul(hv, du_x)));
-        s = dadd(s, dadd(dsub(dsub(dadd(dmul(ls_rr, dh_y), dmul(A.lam_third, de_y)), dmul(lt_r, de_y)),
-                              dmul(A.lam_sixth, de2h_y)),
-                         dmul(lh_omr, db_y)));
-        nv = -s;
-    }
-    {  // vertical velocity (rhs.hpp:196-200)
-        const double hw = dmul(h, w);
-        double s = dmul(0.5, dsub(dsub(dadd(dhuw_x, dmul(hu, dw_x)), dmul(dmul(u, w), dh_x)), dmul(hw, du_x)));
-        s = add_half(s, dsub(dsub(dadd(dhvw_y, dmul(hv, dw_y)), dmul(dmul(v, w), dh_y)), dmul(hw, dv_y)));
-        nw = dsub(dmul(A.lambda, omr), sc(s));
+    if (LIT) {
+        // rhs.hpp:167-200 as written: (0.5*h), (0.5*u), (0.5*hu) ... formed first
+        const double h5 = dmul(0.5, h), u5 = dmul(0.5, u), v5 = dmul(0.5, v);
+        const double hu5 = dmul(0.5, hu), hv5 = dmul(0.5, hv), uv5 = dmul(u5, v);
+        {  // x-momentum
+            double s = dsub(dmul(g, dhhb_x), dmul(ghb, dh_x));
+            s = dadd(s, dsub(dadd(dsub(dmul(h5, du2_x), dmul(dmul(0.5, u2), dh_x)), dmul(u5, dhu_x)),
+                             dmul(hu5, du_x)));
+            s = dadd(s, dsub(dadd(dsub(dmul(0.5, dhuv_y), dmul(uv5, dh_y)), dmul(hv5, du_y)), dmul(hu5, dv_y)));
+            nu = -dadd(s, g3(dh_x, de_x, de2h_x, db_x));
+        }
+        {  // y-momentum
+            double s = dsub(dmul(g, dhhb_y), dmul(ghb, dh_y));
+            s = dadd(s, dsub(dadd(dsub(dmul(h5, dv2_y), dmul(dmul(0.5, v2), dh_y)), dmul(v5, dhv_y)),
+                             dmul(hv5, dv_y)));
+            s = dadd(s, dsub(dadd(dsub(dmul(0.5, dhuv_x), dmul(uv5, dh_x)), dmul(hu5, dv_x)), dmul(hv5, du_x)));
+            nv = -dadd(s, g3(dh_y, de_y, de2h_y, db_y));
+        }
+        {  // vertical velocity
+            const double hw5 = dmul(h5, w);
+            double s = dsub(dsub(dadd(dmul(0.5, dhuw_x), dmul(hu5, dw_x)), dmul(dmul(u5, w), dh_x)), dmul(hw5, du_x));
+            s = dadd(s, dsub(dsub(dadd(dmul(0.5, dhvw_y), dmul(hv5, dw_y)), dmul(dmul(v5, w), dh_y)),
+                             dmul(hw5, dv_y)));
+            nw = dsub(dmul(A.lambda, omr), s);
+        }
+    } else {
+        const double uv = dmul(u, v);
+        {  // x-momentum (rhs.hpp:167-175), 0.5 factored out of the two split groups
+            double s = dsub(dmul(g, dhhb_x), dmul(ghb, dh_x));
+            s = add_half(s, dsub(dadd(dsub(dmul(h, du2_x), dmul(u2, dh_x)), dmul(u, dhu_x)), dmul(hu, du_x)));
+            s = add_half(s, dsub(dadd(dsub(dhuv_y, dmul(uv, dh_y)), dmul(hv, du_y)), dmul(hu, dv_y)));
+            nu = -dadd(s, g3(dh_x, de_x, de2h_x, db_x));
+        }
+        {  // y-momentum (rhs.hpp:180-188)
+            double s = dsub(dmul(g, dhhb_y), dmul(ghb, dh_y));
+            s = add_half(s, dsub(dadd(dsub(dmul(h, dv2_y), dmul(v2, dh_y)), dmul(v, dhv_y)), dmul(hv, dv_y)));
+            s = add_half(s, dsub(dadd(dsub(dhuv_x, dmul(uv, dh_x)), dmul(hu, dv_x)), dmul(hv, du_x)));
+            nv = -dadd(s, g3(dh_y, de_y, de2h_y, db_y));
+        }
+        {  // vertical velocity (rhs.hpp:196-200)
+            const double hw = dmul(h, w);
+            double s =
+                dmul(0.5, dsub(dsub(dadd(dhuw_x, dmul(hu, dw_x)), dmul(dmul(u, w), dh_x)), dmul(hw, du_x)));
+            s = add_half(s, dsub(dsub(dadd(dhvw_y, dmul(hv, dw_y)), dmul(dmul(v, w), dh_y)), dmul(hw, dv_y)));
+            nw = dsub(dmul(A.lambda, omr), sc(s));
+        }
     }
     {  // the three "/h" (rhs.hpp:175,188,200), one range test per node
         bool slow = false;
@@ -480,10 +522,20 @@ __device__ __forceinline__ void tendency(const StageArgs& A, const double2* S, i
     }
 }
 
+// Two-pass tiles: a CTA marches its tile with the
+// fast association and records whether any stage input it formed failed
+// the magnitude guard (lit_node).  If one did (rare: wavefronts entering
+// water at rest), the CTA marches the tile again with the literal
+// association and overwrites its outputs; its inputs are never written by
+// the launch, so the second pass sees the same data.  The counters and
+// reductions are taken from the pass that produced the outputs.  Keeping
+// the literal code in a second loop (not a branch inside the first) leaves
+// the fast loop's register allocation untouched.
+
 // One row of the march: form row jn = j+1 (ring slot SN, register set yn),
 // then finish row j (ring slot SC; row j-1 is register set yp for S2, its
 // ring entry otherwise).
-template <int MODE, int KIND, bool IN, int SC>
+template <int MODE, int KIND, bool IN, bool LIT, int SC>
 __device__ __forceinline__ void march_row(const StageArgs& A, const KPtrs& P, Thr& T, double2* ring, int j0, int j,
                                           const YQ& yp, YQ& yn, Raw& raw, unsigned long long* sbar) {
     constexpr int NP = npairs<MODE>();
@@ -492,15 +544,17 @@ __device__ __forceinline__ void march_row(const StageArgs& A, const KPtrs& P, Th
     const int jn = j + 1;
     const unsigned nx = (unsigned)A.nx;
     {  // products of row jn (for D_y of row j, and D_x of row jn one step later)
-        const bool ok = products<MODE>(A, raw, ring + SN * (NP * BX) + T.tid, yn);
+        bool lit;
+        const bool ok = products<MODE>(A, raw, ring + SN * (NP * BX) + T.tid, yn, lit);
         if (T.finish && jn < T.j1 && !ok) ++T.bad;
+        if (!LIT) T.any |= lit;
     }
     // register prefetch of raw(jn+1), in flight during the finish of row j
     if (jn < T.j1) load_raw<MODE>(P, (unsigned)map_row(A, jn + 1) * nx + T.col, raw);
     // One barrier per row: row j's ring entries (written one step ago) become
     // visible, and this step's writes to slot SN are ordered after the last
     // reads of that slot (finish of row j-2, before the previous barrier).
-    const int t = j - j0 + 1;  // step index (the prologue is step 0)
+    const int t = T.t0 + j - j0 + 1;  // step index (the prologue is step t0)
     if (SPLIT) {
         mbar_wait(&sbar[(t - 1) & 1], (unsigned)((t - 1) >> 1) & 1u);
     } else {
@@ -534,7 +588,8 @@ __device__ __forceinline__ void march_row(const StageArgs& A, const KPtrs& P, Th
         }
     }
     double o[5];
-    tendency<KIND, true, true, IN>(A, S, T.tid, T.sl, T.sr, T.cx, cy, T.xl, T.xr, T.i, j, ypr, yn, Sc[P_RH * BX].x, o);
+    tendency<KIND, true, true, IN, LIT>(A, S, T.tid, T.sl, T.sr, T.cx, cy, T.xl, T.xr, T.i, j, ypr, yn,
+                                        Sc[P_RH * BX].x, o);
     // ---- epilogue
     if (MODE == MODE_S2) {
         const double2 y01 = Sc[P_YP01 * BX], y23 = Sc[P_YP23 * BX], y4 = Sc[P_YP4 * BX];
@@ -572,20 +627,13 @@ __device__ __forceinline__ void march_row(const StageArgs& A, const KPtrs& P, Th
     if (SPLIT) mbar_arrive(&sbar[t & 1]);  // row j finished: its slot may be reused after the next wait
 }
 
-template <int MODE, int KIND, bool IN>
-__global__ void __launch_bounds__(BX, min_blocks<MODE>()) sgn_stage_kernel(const StageArgs A, const KPtrs P) {
-    constexpr int NP = npairs<MODE>();
-    extern __shared__ __align__(16) double2 ring[];  // 3 x NP x BX pairs
-    __shared__ unsigned long long s_min[BX / 32];
-    __shared__ double s_err[BX / 32];
-    __shared__ int s_skip;
-    if (halted(A, &s_skip)) return;
-
-    const int tid = threadIdx.x;
-    const int nx = A.nx, ny = A.ny;
+// Per-thread geometry of this CTA's tile (recomputed by each pass, so
+// that only the accumulators are live across the two passes).
+template <bool IN>
+__device__ __forceinline__ int tile_geo(const StageArgs& A, Thr& T) {
+    const int tid = threadIdx.x, nx = A.nx, ny = A.ny;
     int bx, by;
     tile_of(A, bx, by);
-    Thr T;
     T.tid = tid;
     const int i = bx * WX - 1 + tid;  // logical column (may be -1 or >= nx)
     T.i = i;
@@ -604,25 +652,59 @@ __global__ void __launch_bounds__(BX, min_blocks<MODE>()) sgn_stage_kernel(const
     T.j1 = min(A.band1 > 0 ? A.band1 : ny, j0 + A.rows_per_block);
     T.jc0 = A.y_lo == YE_CLAMP ? 0 : -2;
     T.jc1 = A.y_hi == YE_CLAMP ? ny - 1 : -2;
-    T.bad = 0;
-    T.my_min = ~0ull;
-    T.my_err = 0.0;
-    const unsigned unx = (unsigned)nx;
+    return j0;
+}
 
+// One pass over the tile: prologue (rows j0-1, j0) and the march.
+template <int MODE, int KIND, bool IN, bool LIT>
+__device__ __forceinline__ void march_tile(const StageArgs& A, const KPtrs& P, Thr& T, double2* ring,
+                                           unsigned long long* sbar) {
+    constexpr int NP = npairs<MODE>();
+    const int j0 = tile_geo<IN>(A, T);
+    const unsigned unx = (unsigned)A.nx;
     // ---- prologue: row j0-1 -> register set C (ring slot 2), row j0 -> set A (slot 0)
     YQ ya, yb, yc;
     Raw raw;
+    bool lit;
     load_raw<MODE>(P, (unsigned)map_row(A, j0 - 1) * unx + T.col, raw);
-    products<MODE>(A, raw, ring + 2 * (NP * BX) + tid, yc);
+    products<MODE>(A, raw, ring + 2 * (NP * BX) + T.tid, yc, lit);
+    if (!LIT) T.any |= lit;
     load_raw<MODE>(P, (unsigned)(j0 + 1) * unx + T.col, raw);
     {
-        const bool ok = products<MODE>(A, raw, ring + tid, ya);
+        const bool ok = products<MODE>(A, raw, ring + T.tid, ya, lit);
         if (T.finish && !ok) ++T.bad;
+        if (!LIT) T.any |= lit;
     }
     load_raw<MODE>(P, (unsigned)map_row(A, j0 + 1) * unx + T.col, raw);
-
+    if (split_bar<MODE>()) mbar_arrive(&sbar[T.t0 & 1]);  // step t0: rows j0-1 and j0 written
     // ---- march, unrolled by 3: row j lives in ring slot (j-j0)%3 and register
     // set {a,b,c}[(j-j0)%3]; step SC reads set SC+2 (row j-1), writes SC+1.
+    for (int j = j0; j < T.j1; j += 3) {
+        march_row<MODE, KIND, IN, LIT, 0>(A, P, T, ring, j0, j, yc, yb, raw, sbar);
+        if (j + 1 >= T.j1) break;
+        march_row<MODE, KIND, IN, LIT, 1>(A, P, T, ring, j0, j + 1, ya, yc, raw, sbar);
+        if (j + 2 >= T.j1) break;
+        march_row<MODE, KIND, IN, LIT, 2>(A, P, T, ring, j0, j + 2, yb, ya, raw, sbar);
+    }
+    T.t0 += T.j1 - j0 + 1;  // a second pass continues the barrier phases
+}
+
+template <int MODE, int KIND, bool IN>
+__global__ void __launch_bounds__(BX, min_blocks<MODE>()) sgn_stage_kernel(const StageArgs A, const KPtrs P) {
+    extern __shared__ __align__(16) double2 ring[];  // 3 x NP x BX pairs
+    __shared__ unsigned long long s_min[BX / 32];
+    __shared__ double s_err[BX / 32];
+    __shared__ int s_skip;
+    if (halted(A, &s_skip)) return;
+
+    const int tid = threadIdx.x;
+    Thr T;
+    T.bad = 0;
+    T.my_min = ~0ull;
+    T.my_err = 0.0;
+    T.any = false;
+    T.t0 = 0;
+
     __shared__ __align__(8) unsigned long long sbar[2];
     if (split_bar<MODE>()) {
         if (tid == 0) {
@@ -631,14 +713,17 @@ __global__ void __launch_bounds__(BX, min_blocks<MODE>()) sgn_stage_kernel(const
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         }
         __syncthreads();
-        mbar_arrive(&sbar[0]);  // step 0: rows j0-1 and j0 written
     }
-    for (int j = j0; j < T.j1; j += 3) {
-        march_row<MODE, KIND, IN, 0>(A, P, T, ring, j0, j, yc, yb, raw, sbar);
-        if (j + 1 >= T.j1) break;
-        march_row<MODE, KIND, IN, 1>(A, P, T, ring, j0, j + 1, ya, yc, raw, sbar);
-        if (j + 2 >= T.j1) break;
-        march_row<MODE, KIND, IN, 2>(A, P, T, ring, j0, j + 2, yb, ya, raw, sbar);
+    bool redo = A.lit_all != 0;
+    if (!redo) {
+        march_tile<MODE, KIND, IN, false>(A, P, T, ring, sbar);
+        redo = __syncthreads_or(T.any);
+    }
+    if (redo) {  // literal pass (outputs, counters and partials replaced)
+        T.bad = 0;
+        T.my_min = ~0ull;
+        T.my_err = 0.0;
+        march_tile<MODE, KIND, IN, true>(A, P, T, ring, sbar);
     }
 
     // ---- block reductions (fixed order inside the block)
@@ -696,40 +781,65 @@ __device__ __forceinline__ int map_row2(const StageArgs& A, int jr) {
 #define HSGN_S12_MINB (12 / (BX / 32))
 #endif
 
-// ADAPT: also store the error partial ((d1 k1 + d2 k2) + d3 k3)
-// (time_integration.hpp:128-129, the S2 epilogue of the per-stage path) for
-// the adaptive S3's error norm.
-template <int KIND, bool ADAPT, bool IN>
-__global__ void __launch_bounds__(BX, HSGN_S12_MINB) sgn_s12_kernel(const StageArgs A, const KPtrs P) {
-    extern __shared__ __align__(16) double2 ring[];  // ring A | ring B, each 3 x NPF x BX
-    __shared__ unsigned long long s_min[BX / 32];
-    __shared__ int s_skip;
-    if (halted(A, &s_skip)) return;
-    const int tid = threadIdx.x;
-    const int nx = A.nx, ny = A.ny;
-    // No wall / clamp logic in this CTA: KIND 2 (common factor, only chosen
-    // for fully periodic grids without walls, host-checked) or an interior
-    // tile of a grid with walls
+// Per-thread constants of an S12 tile.
+struct S12Geo {
+    int tid, i, j0, j1, jc0, jc1, sl, sr;
+    bool fa, fb, xl, xr, clamp_lo, clamp_hi;
+    unsigned col;
+    double cx;
+};
+
+struct S12Acc {
+    unsigned bad1, bad2;  // depth failures of this thread's nodes (< 2^32: one column of one strip)
+    unsigned long long my_min;
+    bool any;  // a stage input failed the magnitude guard (fast pass)
+};
+
+// Per-thread geometry of this CTA's S12 tile.  No wall / clamp logic when
+// PER: KIND 2 (common factor, only chosen for fully periodic grids without
+// walls, host-checked) or an interior tile of a grid with walls.
+template <int KIND, bool IN>
+__device__ __forceinline__ S12Geo s12_geo(const StageArgs& A) {
     constexpr bool PER = KIND == 2 || IN;
+    const int tid = threadIdx.x, nx = A.nx, ny = A.ny;
     int bx, by;
     tile_of(A, bx, by);
+    S12Geo G;
+    G.tid = tid;
     const int i = bx * WX2 - 2 + tid;
-    const bool fa = tid >= 1 && tid <= BX - 2 && i >= -1 && i <= nx;  // stage-1 finish
-    const bool fb = tid >= 2 && tid <= BX - 3 && i >= 0 && i < nx;    // stage-2 finish (owned column)
+    G.i = i;
+    G.fa = tid >= 1 && tid <= BX - 2 && i >= -1 && i <= nx;  // stage-1 finish
+    G.fb = tid >= 2 && tid <= BX - 3 && i >= 0 && i < nx;    // stage-2 finish (owned column)
     int c = i;
     if (i < 0) c = (!PER && A.x_bounded) ? 0 : nx + i;
     if (i >= nx) c = ((!PER && A.x_bounded) || i > nx + 1) ? nx - 1 : i - nx;
-    const unsigned col = (unsigned)c;
-    const bool xl = !PER && A.x_bounded && i == 0, xr = !PER && A.x_bounded && i == nx - 1;
-    const double cx = (xl || xr) ? A.c1x : A.cpx;
-    const int sl = xl ? tid : tid - 1, sr = xr ? tid : tid + 1;
-    const int j0 = A.band0 + by * A.rows_per_block;
-    const int j1 = min(A.band1 > 0 ? A.band1 : ny, j0 + A.rows_per_block);
-    const int jc0 = (!PER && A.y_lo == YE_CLAMP) ? 0 : INT_MIN, jc1 = (!PER && A.y_hi == YE_CLAMP) ? ny - 1 : INT_MIN;
-    const bool clamp_lo = !PER && A.y_lo == YE_CLAMP, clamp_hi = !PER && A.y_hi == YE_CLAMP;
-    const unsigned unx = (unsigned)nx;
-    unsigned long long bad1 = 0, bad2 = 0, my_min = ~0ull;
+    G.col = (unsigned)c;
+    G.xl = !PER && A.x_bounded && i == 0;
+    G.xr = !PER && A.x_bounded && i == nx - 1;
+    G.cx = (G.xl || G.xr) ? A.c1x : A.cpx;
+    G.sl = G.xl ? tid : tid - 1;
+    G.sr = G.xr ? tid : tid + 1;
+    G.j0 = A.band0 + by * A.rows_per_block;
+    G.j1 = min(A.band1 > 0 ? A.band1 : ny, G.j0 + A.rows_per_block);
+    G.jc0 = (!PER && A.y_lo == YE_CLAMP) ? 0 : INT_MIN;
+    G.jc1 = (!PER && A.y_hi == YE_CLAMP) ? ny - 1 : INT_MIN;
+    G.clamp_lo = !PER && A.y_lo == YE_CLAMP;
+    G.clamp_hi = !PER && A.y_hi == YE_CLAMP;
+    return G;
+}
 
+// One pass of S12 over the tile.  k: iteration index (split barrier
+// phases), continued by a second pass (which therefore waits from its first
+// iteration on: the fast pass's last phase).
+// ADAPT: also store the error partial ((d1 k1 + d2 k2) + d3 k3)
+// (time_integration.hpp:128-129, the S2 epilogue of the per-stage path) for
+// the adaptive S3's error norm.
+template <int KIND, bool ADAPT, bool IN, bool LIT>
+__device__ __forceinline__ void s12_march(const StageArgs& A, const KPtrs& P, double2* ring,
+                                          unsigned long long* s_bar, int& k, S12Acc& acc) {
+    const S12Geo G = s12_geo<KIND, IN>(A);
+    const int tid = G.tid, i = G.i, j0 = G.j0, j1 = G.j1, ny = A.ny;
+    const unsigned unx = (unsigned)A.nx, col = G.col;
     constexpr int SLOT = NPF * BX;
     // at iteration r ring A holds rows (r-2, r-1, r) in (pa, pb, pc), ring B
     // rows (r-3, r-2, r-1) in (qa, qb, qc); pc and qc are written now
@@ -739,6 +849,7 @@ __global__ void __launch_bounds__(BX, HSGN_S12_MINB) sgn_s12_kernel(const StageA
     double partp[5];                // ((y + c1 k1) + c2 k2) of row r-2
 #pragma unroll
     for (int f = 0; f < 5; ++f) partp[f] = 0.0;
+    bool any = false;
 
     // Split-phase row barrier: iteration k arrives on s_bar[k & 1] after its
     // H2 and iteration k + 1 waits for that phase only after its P1.  P1(r)
@@ -746,28 +857,23 @@ __global__ void __launch_bounds__(BX, HSGN_S12_MINB) sgn_s12_kernel(const StageA
     // across threads in iteration k - 2), so a warp that is ahead forms the
     // next stage-1 input while the others finish.  (Measured slower: a
     // second barrier set with a 4-slot ring B, 2.68 vs 2.63 ms.)
-    __shared__ __align__(8) unsigned long long s_bar[2];
-    if (tid == 0) {
-        for (int q = 0; q < 2; ++q) mbar_init(&s_bar[q], BX);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
     Raw raw;
     load_raw<MODE_S1>(P, (unsigned)map_row2(A, j0 - 2) * unx + col, raw);
-    int k = 0;  // iteration index (split barrier phases)
 #pragma unroll 1
     for (int r = j0 - 2; r <= j1 + 1; ++r, ++k) {
         // ---- P1: stage-1 input of row r (raw of row r+1 loaded right after)
         YQ ya;
         double rhac;
         {
-            const bool ok = products<MODE_S1, false>(A, raw, pc + tid, ya, &rhac);
-            if (fb && r >= j0 && r < j1 && !ok) ++bad1;
+            bool lit;
+            const bool ok = products<MODE_S1, false>(A, raw, pc + tid, ya, lit, &rhac);
+            if (G.fb && r >= j0 && r < j1 && !ok) ++acc.bad1;
+            if (!LIT) any |= lit;
         }
         if (r + 1 <= j1 + 1) load_raw<MODE_S1>(P, (unsigned)map_row2(A, r + 1) * unx + col, raw);
         // H1's own-column inputs need no barrier: they are requested before
         // the wait (this thread loaded them one row ago: L1/L2 hits)
-        const bool do1 = r - 1 >= j0 - 1 && fa;
+        const bool do1 = r - 1 >= j0 - 1 && G.fa;
         double yj[5], kj[5];
         if (do1) {
             const unsigned offj = (unsigned)map_row2(A, r - 1) * unx + col;
@@ -784,34 +890,37 @@ __global__ void __launch_bounds__(BX, HSGN_S12_MINB) sgn_s12_kernel(const StageA
         if (do1) {
             const int j = r - 1;
             YQ yp, yc;
-            neighbour_y((clamp_lo && j == 0 ? pb : pa) + tid, yp);  // a clamped wall row reads itself
-            const bool hi = clamp_hi && j == ny - 1;
+            neighbour_y((G.clamp_lo && j == 0 ? pb : pa) + tid, yp);  // a clamped wall row reads itself
+            const bool hi = G.clamp_hi && j == ny - 1;
             if (hi) neighbour_y(pb + tid, yc);
-            const double cy = (j == jc0 || j == jc1) ? A.c1y : A.cpy;
+            const double cy = (j == G.jc0 || j == G.jc1) ? A.c1y : A.cpy;
             double k2[5];
-            tendency<KIND, false, false, IN>(A, pb, tid, sl, sr, cx, cy, xl, xr, i, j, yp, hi ? yc : ya, rhap, k2);
+            tendency<KIND, false, false, IN, LIT>(A, pb, tid, G.sl, G.sr, G.cx, cy, G.xl, G.xr, i, j, yp,
+                                                  hi ? yc : ya, rhap, k2);
             double q[5];
 #pragma unroll
             for (int f = 0; f < 5; ++f) {
                 q[f] = dadd(yj[f], dmul(A.a2, k2[f]));                                  // state_add1
                 partc[f] = dadd(dadd(yj[f], dmul(A.c1, kj[f])), dmul(A.c2, k2[f]));  // state_add3, 2 terms
             }
-            if (ADAPT && fb && j >= j0 && j < j1) {  // d1 k1 + d2 k2 of row j, completed by H2 one row later
+            if (ADAPT && G.fb && j >= j0 && j < j1) {  // d1 k1 + d2 k2 of row j, completed by H2 one row later
                 const unsigned offe = (unsigned)(j + GHOST) * unx + col;
 #pragma unroll
                 for (int f = 0; f < 5; ++f) P.part[f][offe] = dadd(dmul(A.d1, kj[f]), dmul(A.d2, k2[f]));
             }
-            const bool ok = products_q<false>(q, pb[tid + P_EB * BX].y, qc + tid, yb, &rhbc);
-            if (fb && j >= j0 && j < j1 && !ok) ++bad2;
+            bool lit;
+            const bool ok = products_q<false>(q, pb[tid + P_EB * BX].y, qc + tid, yb, &rhbc, lit);
+            if (G.fb && j >= j0 && j < j1 && !ok) ++acc.bad2;
+            if (!LIT) any |= lit;
         }
         // ---- H2: k3 at row r-2 -> ynew (stored, min h)
-        if (r - 2 >= j0 && fb) {
+        if (r - 2 >= j0 && G.fb) {
             const int j = r - 2;
             YQ yp, yc;
-            neighbour_y((clamp_lo && j == 0 ? qb : qa) + tid, yp);
-            const bool hi = clamp_hi && j == ny - 1;
+            neighbour_y((G.clamp_lo && j == 0 ? qb : qa) + tid, yp);
+            const bool hi = G.clamp_hi && j == ny - 1;
             if (hi) neighbour_y(qb + tid, yc);
-            const double cy = (j == jc0 || j == jc1) ? A.c1y : A.cpy;
+            const double cy = (j == G.jc0 || j == G.jc1) ? A.c1y : A.cpy;
             const unsigned off = (unsigned)(j + GHOST) * unx + col;
             double e12[5];  // ADAPT: d1 k1 + d2 k2 stored by H1 one row ago (requested before the tendency)
             if (ADAPT) {
@@ -819,7 +928,8 @@ __global__ void __launch_bounds__(BX, HSGN_S12_MINB) sgn_s12_kernel(const StageA
                 for (int f = 0; f < 5; ++f) e12[f] = P.part[f][off];
             }
             double k3[5];
-            tendency<KIND, false, false, IN>(A, qb, tid, sl, sr, cx, cy, xl, xr, i, j, yp, hi ? yc : yb, rhbp, k3);
+            tendency<KIND, false, false, IN, LIT>(A, qb, tid, G.sl, G.sr, G.cx, cy, G.xl, G.xr, i, j, yp,
+                                                  hi ? yc : yb, rhbp, k3);
 #pragma unroll
             for (int f = 0; f < 5; ++f) P.out[f][off] = dadd(partp[f], dmul(A.c3, k3[f]));  // state_add3
             if (ADAPT) {  // ((d1 k1 + d2 k2) + d3 k3) (time_integration.hpp:128-129)
@@ -828,7 +938,7 @@ __global__ void __launch_bounds__(BX, HSGN_S12_MINB) sgn_s12_kernel(const StageA
             }
             const unsigned long long bits =
                 (unsigned long long)__double_as_longlong(dadd(partp[0], dmul(A.c3, k3[0])));
-            my_min = bits < my_min ? bits : my_min;
+            acc.my_min = bits < acc.my_min ? bits : acc.my_min;
         }
         mbar_arrive(&s_bar[k & 1]);
         // ---- rotate
@@ -845,10 +955,37 @@ __global__ void __launch_bounds__(BX, HSGN_S12_MINB) sgn_s12_kernel(const StageA
 #pragma unroll
         for (int f = 0; f < 5; ++f) partp[f] = partc[f];
     }
-    if (bad1) atomicAdd(A.bad, bad1);
-    if (bad2) atomicAdd(A.bad2, bad2);
+    if (!LIT) acc.any = any;
+}
+
+template <int KIND, bool ADAPT, bool IN>
+__global__ void __launch_bounds__(BX, HSGN_S12_MINB) sgn_s12_kernel(const StageArgs A, const KPtrs P) {
+    extern __shared__ __align__(16) double2 ring[];  // ring A | ring B, each 3 x NPF x BX
+    __shared__ unsigned long long s_min[BX / 32];
+    __shared__ int s_skip;
+    if (halted(A, &s_skip)) return;
+    const int tid = threadIdx.x;
+    __shared__ __align__(8) unsigned long long s_bar[2];
+    if (tid == 0) {
+        for (int q = 0; q < 2; ++q) mbar_init(&s_bar[q], BX);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    S12Acc acc{0u, 0u, ~0ull, false};
+    int k = 0;
+    bool redo = A.lit_all != 0;
+    if (!redo) {
+        s12_march<KIND, ADAPT, IN, false>(A, P, ring, s_bar, k, acc);
+        redo = __syncthreads_or(acc.any);
+    }
+    if (redo) {  // literal pass (outputs, counters and min replaced)
+        acc = S12Acc{0u, 0u, ~0ull, false};
+        s12_march<KIND, ADAPT, IN, true>(A, P, ring, s_bar, k, acc);
+    }
+    if (acc.bad1) atomicAdd(A.bad, (unsigned long long)acc.bad1);
+    if (acc.bad2) atomicAdd(A.bad2, (unsigned long long)acc.bad2);
     if (A.minh) {
-        const unsigned long long m = warp_min_u64(my_min);
+        const unsigned long long m = warp_min_u64(acc.my_min);
         if ((tid & 31) == 0) s_min[tid >> 5] = m;
         __syncthreads();
         if (tid == 0) {
