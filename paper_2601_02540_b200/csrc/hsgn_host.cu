@@ -98,7 +98,7 @@ const NcclApi& nccl() {
 }
 constexpr int NCCL_UINT64 = 5;   // ncclUint64
 constexpr int NCCL_FLOAT64 = 8;  // ncclDouble
-constexpr int NCCL_SUM = 0, NCCL_MIN = 3;
+constexpr int NCCL_SUM = 0, NCCL_MAX = 2, NCCL_MIN = 3;
 }  // namespace
 
 // ------------------------------------------------------------------ types
@@ -139,6 +139,9 @@ struct hsgn_ctx {
     int forced_kind = -1;  // stencil kind override (tests); -1 = automatic
     int in_group = 0;      // member of an in-process slab group (halo pulls by the group)
     int ring1 = 0;         // 1-slab ring: NCCL attached to a 1-rank periodic-y context (halos to itself)
+    int b_lit = 0;         // some b value (of any slab) outside the magnitude guard (sgn_device.cuh)
+    int* d_hint = nullptr; // literal-pass tile hints (StageArgs::hint_s12 / hint_stage)
+    long long hint_cap = 0;
     int fused = 3;         // fixed-step structure: 0 one kernel per stage, 3 S12 + S3
     int64_t n_evals = 0;
     int64_t launches = 0;  // kernels of this library launched (or captured) on the context stream
@@ -320,8 +323,9 @@ static hsgn_status setup_ctx(hsgn_ctx* c) {
     // magnitude guard of the fast association (sgn_device.cuh lit_node): the
     // constants must be zero or in [2^-60, 2^60], else every row is literal
     auto guard_ok = [](double x) { return x == 0.0 || (std::fabs(x) >= 0x1p-60 && std::fabs(x) <= 0x1p60); };
-    A.lit_all = !(guard_ok(c->phys.g) && guard_ok(c->phys.lambda) && guard_ok(A.cpx) && guard_ok(A.cpy) &&
-                  guard_ok(A.c1x) && guard_ok(A.c1y) && guard_ok(A.tdx) && guard_ok(A.tdy));
+    // (b, g and lambda matter only under the common factor, stencil kind 2)
+    A.lit_all = !(guard_ok(A.cpx) && guard_ok(A.cpy) && guard_ok(A.c1x) && guard_ok(A.c1y)) ||
+                (A.pow2 == 2 && (c->b_lit || !guard_ok(c->phys.g) || !guard_ok(c->phys.lambda)));
 #ifdef HSGN_FORCE_LIT
     A.lit_all = 1;  // experiments: literal association everywhere
 #endif
@@ -344,6 +348,19 @@ static hsgn_status setup_ctx(hsgn_ctx* c) {
         int rpb = 128;
         while (rpb > 16 && (long long)tiles_x * ((c->ny_loc + rpb - 1) / rpb) < 148LL * 3 * 6) rpb /= 2;
         A.rows_per_block = rpb;
+    }
+    {  // literal-pass tile hints: one int per CTA of a whole-slab S12 / per-stage launch
+        const long long nb = (c->ny_loc + A.rows_per_block - 1) / A.rows_per_block;
+        const long long n12 = (g.nx + 123) / 124 * nb, nst = (g.nx + 125) / 126 * nb;
+        if (n12 + nst > c->hint_cap) {
+            if (c->d_hint) cudaFree(c->d_hint);
+            c->d_hint = nullptr;
+            c->hint_cap = 0;
+            if (cudaMalloc(&c->d_hint, sizeof(int) * (n12 + nst)) == cudaSuccess) c->hint_cap = n12 + nst;
+        }
+        if (c->d_hint) cudaMemset(c->d_hint, 0, sizeof(int) * c->hint_cap);
+        A.hint_s12 = c->d_hint;
+        A.hint_stage = c->d_hint ? c->d_hint + n12 : nullptr;
     }
     AuxArgs& X = c->aux;
     X.nx = g.nx;
@@ -857,6 +874,7 @@ static hsgn_status create_common(const hsgn_grid* grid, const hsgn_phys* phys, c
     }
     const int ny_loc = j_end - j_begin;
     const long long fsz = (long long)(ny_loc + 2 * GHOST) * grid->nx;
+    c->b_lit = b_needs_literal(b_host, (long long)ny_loc * grid->nx);
     e = cudaMalloc(&c->b_alloc, sizeof(double) * fsz);
     if (e == cudaSuccess) {
         c->b = c->b_alloc + GHOST * grid->nx;
@@ -930,6 +948,20 @@ hsgn_status hsgn_ctx_attach_nccl(hsgn_ctx* c, const unsigned char nccl_id[128]) 
     bs.fs = c->fs;
     hsgn_status s = exchange(c, &bs, 1);
     if (s) return s;
+    if (multi_rank(c)) {  // the guard's b flag covers every slab (ghost rows come from the neighbours)
+        if ((s = ensure_recs(c, 0))) return s;  // d_scalar
+        double* d = c->d_scalar;
+        const double f = c->b_lit;
+        CK(cudaMemcpyAsync(d, &f, sizeof f, cudaMemcpyHostToDevice, c->stream));
+        if ((s = agree(c, d, 1, NCCL_FLOAT64, NCCL_MAX))) return s;
+        double g = 0.0;
+        CK(cudaMemcpyAsync(&g, d, sizeof g, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        if (g != 0.0 && !c->b_lit) {
+            c->b_lit = 1;
+            setup_ctx(c);
+        }
+    }
     CK(cudaStreamSynchronize(c->stream));
     return HSGN_OK;
 }
@@ -948,6 +980,7 @@ hsgn_status hsgn_ctx_destroy(hsgn_ctx* c) {
     if (c->d_halt) cudaFree(c->d_halt);
     if (c->d_err_part) cudaFree(c->d_err_part);
     if (c->d_scalar) cudaFree(c->d_scalar);
+    if (c->d_hint) cudaFree(c->d_hint);
     if (c->d_rows) cudaFree(c->d_rows);
     if (c->h_rows) cudaFreeHost(c->h_rows);
     if (c->ev0) cudaEventDestroy(c->ev0);
@@ -2104,6 +2137,13 @@ hsgn_status hsgn_group_create(const hsgn_grid* grid, const hsgn_phys* phys, cons
     }
     hsgn_status s = group_pull(G, bs, 1);
     for (int r = 0; r < n; ++r) cudaStreamSynchronize(G->m[r]->stream);
+    int b_lit = 0;  // the guard's b flag covers every slab
+    for (int r = 0; r < n; ++r) b_lit |= G->m[r]->b_lit;
+    for (int r = 0; r < n && b_lit; ++r)
+        if (!G->m[r]->b_lit) {
+            G->m[r]->b_lit = 1;
+            setup_ctx(G->m[r]);
+        }
     if (s) {
         hsgn_group_destroy(G);
         return s;

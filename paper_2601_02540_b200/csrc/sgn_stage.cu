@@ -79,23 +79,28 @@ struct YQ {  // y-differentiated quantities of one row at this column (rhs.hpp:1
 };
 
 // Tile coordinates of this CTA.  A.tile_mode 0: the
-// plain grid; 1: the interior grid (offset past the leading edge column
-// tiles and edge strips); 2: the edge tiles, enumerated as the leading /
-// trailing edge strips (all column tiles) followed by the leading /
-// trailing edge column tiles of every remaining strip.
+// plain grid (blockIdx = tile); 1: one launch over the edge tiles and then
+// the interior tiles of a grid with walls: CTAs [0, n_edge) take the edge
+// tiles, enumerated as the leading / trailing edge strips (all column tiles)
+// followed by the leading / trailing edge column tiles of every remaining
+// strip; CTAs from n_edge on take the interior tiles row by row.
+__device__ __forceinline__ bool edge_cta(const StageArgs& A) { return A.tile_mode == 1 && (int)blockIdx.x < A.n_edge; }
+
 __device__ __forceinline__ void tile_of(const StageArgs& A, int& bx, int& by) {
     if (A.tile_mode == 0) {
         bx = blockIdx.x;
         by = blockIdx.y;
         return;
     }
-    if (A.tile_mode == 1) {
-        bx = blockIdx.x + A.ex_lo;
-        by = blockIdx.y + A.ey_lo;
-        return;
-    }
     int k = blockIdx.x;
     const int ntx = A.ntx, nby = A.nby;
+    if (k >= A.n_edge) {  // interior tile
+        k -= A.n_edge;
+        const int gx = ntx - A.ex_lo - A.ex_hi;
+        bx = A.ex_lo + k % gx;
+        by = A.ey_lo + k / gx;
+        return;
+    }
     if (k < A.ey_lo * ntx) {
         bx = k % ntx;
         by = k / ntx;
@@ -142,13 +147,13 @@ __device__ __forceinline__ void load_raw(const KPtrs& P, unsigned off, Raw& r) {
 // Pointwise products of rhs.hpp:99-109 at one node from the stage input q
 // (h, u, v, w, eta) and b: stores the ring pairs of the node (S already
 // offset by ring row and column), fills the y-quantities and the node's
-// magnitude-guard flag (lit_node); returns h > 0.
-template <bool STORE_RH = true>
+// magnitude guard (guard_add); returns h > 0.
+template <int KIND, bool STORE_RH = true>
 __device__ __forceinline__ bool products_q(const double q[5], double b, double2* S, YQ& Y, double* rh_out,
-                                           bool& lit) {
+                                           Guard& gd) {
     const double h = q[0], u = q[1], v = q[2], w = q[3], e = q[4];
     const bool ok = h > 0.0;
-    lit = lit_node(q, b);
+    guard_add<KIND>(gd, q);
     const double rh = rcp_or_nan(h);
     bool slow = false;
     double r = div_fast(e, h, rh, slow);  // eta/h computed once (rhs.hpp:86-88)
@@ -179,14 +184,14 @@ __device__ __forceinline__ bool products_q(const double q[5], double b, double2*
 // The same from raw stage data: q = y + a*k (state_add1,
 // time_integration.hpp:61-75) for S1/S2, q = y otherwise; S2 also stores
 // ((y + c1 k1) + c2 k2), the k3-free part of ynew (state_add3).
-template <int MODE, bool STORE_RH = true>
-__device__ __forceinline__ bool products(const StageArgs& A, const Raw& raw, double2* S, YQ& Y, bool& lit,
+template <int MODE, int KIND, bool STORE_RH = true>
+__device__ __forceinline__ bool products(const StageArgs& A, const Raw& raw, double2* S, YQ& Y, Guard& gd,
                                          double* rh_out = nullptr) {
     double q[5];
 #pragma unroll
     for (int f = 0; f < 5; ++f)
         q[f] = (MODE == MODE_S1 || MODE == MODE_S2) ? dadd(raw.y[f], dmul(A.a, raw.k[f])) : raw.y[f];
-    const bool ok = products_q<STORE_RH>(q, raw.b, S, Y, rh_out, lit);
+    const bool ok = products_q<KIND, STORE_RH>(q, raw.b, S, Y, rh_out, gd);
     if (MODE == MODE_S2) {
         double yp[5];
 #pragma unroll
@@ -320,7 +325,7 @@ struct Thr {
     int jc0, jc1;       // rows that use the y closure coefficient (clamped walls)
     unsigned long long bad, my_min;
     double my_err;
-    bool any;           // fast pass: a stage input this thread formed failed the magnitude guard
+    Guard gd;           // fast pass: magnitude guard over the stage inputs this thread formed
     int t0;             // split-barrier step index of this pass's prologue
 };
 
@@ -544,10 +549,8 @@ __device__ __forceinline__ void march_row(const StageArgs& A, const KPtrs& P, Th
     const int jn = j + 1;
     const unsigned nx = (unsigned)A.nx;
     {  // products of row jn (for D_y of row j, and D_x of row jn one step later)
-        bool lit;
-        const bool ok = products<MODE>(A, raw, ring + SN * (NP * BX) + T.tid, yn, lit);
+        const bool ok = products<MODE, KIND>(A, raw, ring + SN * (NP * BX) + T.tid, yn, T.gd);
         if (T.finish && jn < T.j1 && !ok) ++T.bad;
-        if (!LIT) T.any |= lit;
     }
     // register prefetch of raw(jn+1), in flight during the finish of row j
     if (jn < T.j1) load_raw<MODE>(P, (unsigned)map_row(A, jn + 1) * nx + T.col, raw);
@@ -665,15 +668,12 @@ __device__ __forceinline__ void march_tile(const StageArgs& A, const KPtrs& P, T
     // ---- prologue: row j0-1 -> register set C (ring slot 2), row j0 -> set A (slot 0)
     YQ ya, yb, yc;
     Raw raw;
-    bool lit;
     load_raw<MODE>(P, (unsigned)map_row(A, j0 - 1) * unx + T.col, raw);
-    products<MODE>(A, raw, ring + 2 * (NP * BX) + T.tid, yc, lit);
-    if (!LIT) T.any |= lit;
+    products<MODE, KIND>(A, raw, ring + 2 * (NP * BX) + T.tid, yc, T.gd);
     load_raw<MODE>(P, (unsigned)(j0 + 1) * unx + T.col, raw);
     {
-        const bool ok = products<MODE>(A, raw, ring + T.tid, ya, lit);
+        const bool ok = products<MODE, KIND>(A, raw, ring + T.tid, ya, T.gd);
         if (T.finish && !ok) ++T.bad;
-        if (!LIT) T.any |= lit;
     }
     load_raw<MODE>(P, (unsigned)map_row(A, j0 + 1) * unx + T.col, raw);
     if (split_bar<MODE>()) mbar_arrive(&sbar[T.t0 & 1]);  // step t0: rows j0-1 and j0 written
@@ -690,22 +690,15 @@ __device__ __forceinline__ void march_tile(const StageArgs& A, const KPtrs& P, T
 }
 
 template <int MODE, int KIND, bool IN>
-__global__ void __launch_bounds__(BX, min_blocks<MODE>()) sgn_stage_kernel(const StageArgs A, const KPtrs P) {
-    extern __shared__ __align__(16) double2 ring[];  // 3 x NP x BX pairs
-    __shared__ unsigned long long s_min[BX / 32];
-    __shared__ double s_err[BX / 32];
-    __shared__ int s_skip;
-    if (halted(A, &s_skip)) return;
-
+__device__ __forceinline__ void stage_body(const StageArgs& A, const KPtrs& P, double2* ring, unsigned long long* s_min,
+                                           double* s_err, unsigned long long* sbar) {
     const int tid = threadIdx.x;
     Thr T;
     T.bad = 0;
     T.my_min = ~0ull;
     T.my_err = 0.0;
-    T.any = false;
     T.t0 = 0;
 
-    __shared__ __align__(8) unsigned long long sbar[2];
     if (split_bar<MODE>()) {
         if (tid == 0) {
             mbar_init(&sbar[0], BX);
@@ -714,17 +707,25 @@ __global__ void __launch_bounds__(BX, min_blocks<MODE>()) sgn_stage_kernel(const
         }
         __syncthreads();
     }
-    bool redo = A.lit_all != 0;
+    // literal-pass hint of this tile (set when its last launch needed the
+    // literal pass: a front stays in a tile for many steps)
+    int* hint = A.hint_stage ? A.hint_stage + blockIdx.y * gridDim.x + blockIdx.x : nullptr;
+    const bool hinted = !A.lit_all && hint && *hint;
+    bool redo = A.lit_all || hinted;
     if (!redo) {
         march_tile<MODE, KIND, IN, false>(A, P, T, ring, sbar);
-        redo = __syncthreads_or(T.any);
+        redo = __syncthreads_or(guard_fail(T.gd));
     }
+    bool need = false;
     if (redo) {  // literal pass (outputs, counters and partials replaced)
         T.bad = 0;
         T.my_min = ~0ull;
         T.my_err = 0.0;
+        T.gd = Guard();
         march_tile<MODE, KIND, IN, true>(A, P, T, ring, sbar);
+        if (hint) need = __syncthreads_or(guard_fail(T.gd));
     }
+    if (hint && tid == 0 && need != hinted) *hint = need;
 
     // ---- block reductions (fixed order inside the block)
     if (T.bad) atomicAdd(A.bad, T.bad);
@@ -746,9 +747,26 @@ __global__ void __launch_bounds__(BX, min_blocks<MODE>()) sgn_stage_kernel(const
         if (tid == 0) {
             double t = 0.0;
             for (int k = 0; k < BX / 32; ++k) t = dadd(t, s_err[k]);
-            A.err_part[A.part_base + blockIdx.y * gridDim.x + blockIdx.x] = t;
+            A.err_part[blockIdx.y * gridDim.x + blockIdx.x] = t;
         }
     }
+}
+
+// TILES 0: every tile general (IN = false); 1: every tile interior (no
+// walls, or KIND 2); 2: one launch over edge tiles (general) and interior
+// tiles (tile_mode 1, see tile_of).
+template <int MODE, int KIND, int TILES>
+__global__ void __launch_bounds__(BX, min_blocks<MODE>()) sgn_stage_kernel(const StageArgs A, const KPtrs P) {
+    extern __shared__ __align__(16) double2 ring[];  // 3 x NP x BX pairs
+    __shared__ unsigned long long s_min[BX / 32];
+    __shared__ double s_err[BX / 32];
+    __shared__ __align__(8) unsigned long long sbar[2];
+    __shared__ int s_skip;
+    if (halted(A, &s_skip)) return;
+    if (TILES == 1 || (TILES == 2 && !edge_cta(A)))
+        stage_body<MODE, KIND, true>(A, P, ring, s_min, s_err, sbar);
+    else
+        stage_body<MODE, KIND, false>(A, P, ring, s_min, s_err, sbar);
 }
 
 // Fused kernels: memory row of -GHOST <= jr < ny + GHOST, counted from row
@@ -790,9 +808,9 @@ struct S12Geo {
 };
 
 struct S12Acc {
-    unsigned bad1, bad2;  // depth failures of this thread's nodes (< 2^32: one column of one strip)
+    unsigned* bad;        // shared per-CTA depth-failure counters of stages 1, 2 (incremented on failure only)
     unsigned long long my_min;
-    bool any;  // a stage input failed the magnitude guard (fast pass)
+    bool any;  // fast pass: a stage input failed the magnitude guard
 };
 
 // Per-thread geometry of this CTA's S12 tile.  No wall / clamp logic when
@@ -849,7 +867,7 @@ __device__ __forceinline__ void s12_march(const StageArgs& A, const KPtrs& P, do
     double partp[5];                // ((y + c1 k1) + c2 k2) of row r-2
 #pragma unroll
     for (int f = 0; f < 5; ++f) partp[f] = 0.0;
-    bool any = false;
+    Guard gd;
 
     // Split-phase row barrier: iteration k arrives on s_bar[k & 1] after its
     // H2 and iteration k + 1 waits for that phase only after its P1.  P1(r)
@@ -865,10 +883,8 @@ __device__ __forceinline__ void s12_march(const StageArgs& A, const KPtrs& P, do
         YQ ya;
         double rhac;
         {
-            bool lit;
-            const bool ok = products<MODE_S1, false>(A, raw, pc + tid, ya, lit, &rhac);
-            if (G.fb && r >= j0 && r < j1 && !ok) ++acc.bad1;
-            if (!LIT) any |= lit;
+            const bool ok = products<MODE_S1, KIND, false>(A, raw, pc + tid, ya, gd, &rhac);
+            if (G.fb && r >= j0 && r < j1 && !ok) atomicAdd(&acc.bad[0], 1u);
         }
         if (r + 1 <= j1 + 1) load_raw<MODE_S1>(P, (unsigned)map_row2(A, r + 1) * unx + col, raw);
         // H1's own-column inputs need no barrier: they are requested before
@@ -908,10 +924,8 @@ __device__ __forceinline__ void s12_march(const StageArgs& A, const KPtrs& P, do
 #pragma unroll
                 for (int f = 0; f < 5; ++f) P.part[f][offe] = dadd(dmul(A.d1, kj[f]), dmul(A.d2, k2[f]));
             }
-            bool lit;
-            const bool ok = products_q<false>(q, pb[tid + P_EB * BX].y, qc + tid, yb, &rhbc, lit);
-            if (G.fb && j >= j0 && j < j1 && !ok) ++acc.bad2;
-            if (!LIT) any |= lit;
+            const bool ok = products_q<KIND, false>(q, pb[tid + P_EB * BX].y, qc + tid, yb, &rhbc, gd);
+            if (G.fb && j >= j0 && j < j1 && !ok) atomicAdd(&acc.bad[1], 1u);
         }
         // ---- H2: k3 at row r-2 -> ynew (stored, min h)
         if (r - 2 >= j0 && G.fb) {
@@ -955,35 +969,45 @@ __device__ __forceinline__ void s12_march(const StageArgs& A, const KPtrs& P, do
 #pragma unroll
         for (int f = 0; f < 5; ++f) partp[f] = partc[f];
     }
-    if (!LIT) acc.any = any;
+    acc.any = guard_fail(gd);
 }
 
 template <int KIND, bool ADAPT, bool IN>
-__global__ void __launch_bounds__(BX, HSGN_S12_MINB) sgn_s12_kernel(const StageArgs A, const KPtrs P) {
-    extern __shared__ __align__(16) double2 ring[];  // ring A | ring B, each 3 x NPF x BX
-    __shared__ unsigned long long s_min[BX / 32];
-    __shared__ int s_skip;
-    if (halted(A, &s_skip)) return;
+__device__ __forceinline__ void s12_body(const StageArgs& A, const KPtrs& P, double2* ring, unsigned long long* s_min,
+                                         unsigned long long* s_bar) {
     const int tid = threadIdx.x;
-    __shared__ __align__(8) unsigned long long s_bar[2];
     if (tid == 0) {
         for (int q = 0; q < 2; ++q) mbar_init(&s_bar[q], BX);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    S12Acc acc{0u, 0u, ~0ull, false};
+    __shared__ unsigned s_bad[2];
+    if (tid < 2) s_bad[tid] = 0u;
+    __syncthreads();
+    S12Acc acc{s_bad, ~0ull, false};
     int k = 0;
-    bool redo = A.lit_all != 0;
+    // literal-pass hint of this tile (see stage_body)
+    int* hint = A.hint_s12 ? A.hint_s12 + blockIdx.y * gridDim.x + blockIdx.x : nullptr;
+    const bool hinted = !A.lit_all && hint && *hint;
+    bool redo = A.lit_all || hinted;
     if (!redo) {
         s12_march<KIND, ADAPT, IN, false>(A, P, ring, s_bar, k, acc);
         redo = __syncthreads_or(acc.any);
+        if (redo) {  // the fast pass's counts are discarded
+            if (tid < 2) s_bad[tid] = 0u;
+            __syncthreads();
+        }
     }
+    bool need = false;
     if (redo) {  // literal pass (outputs, counters and min replaced)
-        acc = S12Acc{0u, 0u, ~0ull, false};
+        acc = S12Acc{s_bad, ~0ull, false};
         s12_march<KIND, ADAPT, IN, true>(A, P, ring, s_bar, k, acc);
+        if (hint) need = __syncthreads_or(acc.any);
     }
-    if (acc.bad1) atomicAdd(A.bad, (unsigned long long)acc.bad1);
-    if (acc.bad2) atomicAdd(A.bad2, (unsigned long long)acc.bad2);
+    if (hint && tid == 0 && need != hinted) *hint = need;
+    __syncthreads();
+    if (tid == 0 && s_bad[0]) atomicAdd(A.bad, (unsigned long long)s_bad[0]);
+    if (tid == 0 && s_bad[1]) atomicAdd(A.bad2, (unsigned long long)s_bad[1]);
     if (A.minh) {
         const unsigned long long m = warp_min_u64(acc.my_min);
         if ((tid & 31) == 0) s_min[tid >> 5] = m;
@@ -994,6 +1018,19 @@ __global__ void __launch_bounds__(BX, HSGN_S12_MINB) sgn_s12_kernel(const StageA
             if (mm != ~0ull) atomicMin(A.minh, mm);
         }
     }
+}
+
+template <int KIND, bool ADAPT, int TILES>
+__global__ void __launch_bounds__(BX, HSGN_S12_MINB) sgn_s12_kernel(const StageArgs A, const KPtrs P) {
+    extern __shared__ __align__(16) double2 ring[];  // ring A | ring B, each 3 x NPF x BX
+    __shared__ unsigned long long s_min[BX / 32];
+    __shared__ __align__(8) unsigned long long s_bar[2];
+    __shared__ int s_skip;
+    if (halted(A, &s_skip)) return;
+    if (TILES == 1 || (TILES == 2 && !edge_cta(A)))
+        s12_body<KIND, ADAPT, true>(A, P, ring, s_min, s_bar);
+    else
+        s12_body<KIND, ADAPT, false>(A, P, ring, s_min, s_bar);
 }
 
 // Deterministic final sum of per-block partials (single CTA, fixed order,
@@ -1090,49 +1127,53 @@ static TileSplit tile_split(const StageArgs& A, int wx, int hx, int reach) {
     return s;
 }
 
-// Launch `kernel_in` over the interior tiles and `kernel_ed` over the edge
-// tiles of one stage.  The edge launch (fewer tiles than one wave at the
-// benchmark sizes) goes first.  `per_block`: S3A partial index base.
-template <class KIn, class KEd>
-static cudaError_t launch_split(StageArgs A, const KPtrs& P, KIn kernel_in, KEd kernel_ed, size_t smem, int wx,
-                                int hx, int reach, cudaStream_t st) {
+// Tile plan of one launch: 0 every tile general,
+// 1 every tile interior, 2 edge tiles then interior tiles (tile_mode 1).
+static int tile_plan(StageArgs& A, int wx, int hx, int reach, dim3& grid) {
     const TileSplit s = tile_split(A, wx, hx, reach);
     A.ntx = s.ntx;
     A.nby = s.nby;
-    if (s.n_edge < 0) {  // no separable interior: the general instance everywhere
-        A.tile_mode = 0;
-        kernel_ed<<<dim3(s.ntx, s.nby), BX, smem, st>>>(A, P);
-        return cudaGetLastError();
-    }
+    A.tile_mode = 0;
+    grid = dim3(s.ntx, s.nby);
+    if (s.n_edge < 0) return 0;   // no separable interior: the general instance everywhere
+    if (s.n_edge == 0) return 1;  // no closure nodes
     A.ex_lo = s.ex_lo;
     A.ex_hi = s.ex_hi;
     A.ey_lo = s.ey_lo;
     A.ey_hi = s.ey_hi;
-    int base = 0;
-    if (s.n_edge > 0) {
-        A.tile_mode = 2;
-        A.part_base = 0;
-        kernel_ed<<<dim3(s.n_edge, 1), BX, smem, st>>>(A, P);
-        base = s.n_edge;
-        const cudaError_t e = cudaGetLastError();
-        if (e != cudaSuccess) return e;
+    A.n_edge = s.n_edge;
+    A.tile_mode = 1;
+    grid = dim3(s.ntx * s.nby, 1);  // edge CTAs first: the slower tiles start in the first wave
+    return 2;
+}
+
+// Launch kernel instance K<plan> for the tile plan of these arguments,
+// opting each instance in to its dynamic shared memory on first use.  KIND 2
+// grids have no closure nodes (host-checked), so only plan 1 exists for them.
+template <int KIND, class K0, class K1, class K2>
+static cudaError_t launch_planned(const StageArgs& A, const KPtrs& P, K0 k0, K1 k1, K2 k2, unsigned long long* opted,
+                                  size_t smem, int wx, int hx, int reach, cudaStream_t st) {
+    StageArgs B = A;
+    dim3 grid;
+    const int plan = tile_plan(B, wx, hx, reach, grid);
+    cudaError_t e = cudaSuccess;
+    if (plan == 1 || KIND == 2) {
+        e = smem_opt_in(opted[1], k1, smem);
+        if (e == cudaSuccess) k1<<<grid, BX, smem, st>>>(B, P);
+    } else if (plan == 0) {
+        e = smem_opt_in(opted[0], k0, smem);
+        if (e == cudaSuccess) k0<<<grid, BX, smem, st>>>(B, P);
+    } else {
+        e = smem_opt_in(opted[2], k2, smem);
+        if (e == cudaSuccess) k2<<<grid, BX, smem, st>>>(B, P);
     }
-    const int gx = s.ntx - s.ex_lo - s.ex_hi, gy = s.nby - s.ey_lo - s.ey_hi;
-    if (gx > 0 && gy > 0) {
-        A.tile_mode = s.n_edge > 0 ? 1 : 0;
-        A.part_base = base;
-        kernel_in<<<dim3(gx, gy), BX, smem, st>>>(A, P);
-    }
-    return cudaGetLastError();
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 template <int MODE, int KIND>
 static cudaError_t launch_mode(const StageArgs& A, cudaStream_t st) {
-    static unsigned long long opted_in = 0, opted_ed = 0;
+    static unsigned long long opted[3] = {0, 0, 0};
     constexpr size_t bytes = ring_bytes<MODE>();
-    cudaError_t e = smem_opt_in(opted_in, sgn_stage_kernel<MODE, KIND, true>, bytes);
-    if (e == cudaSuccess) e = smem_opt_in(opted_ed, sgn_stage_kernel<MODE, KIND, false>, bytes);
-    if (e != cudaSuccess) return e;
     KPtrs P;  // field bases at the ghost row -1 (see map_row)
     const long long g = A.nx;
     for (int f = 0; f < 5; ++f) {
@@ -1144,19 +1185,18 @@ static cudaError_t launch_mode(const StageArgs& A, cudaStream_t st) {
         P.yold[f] = A.yold ? A.yold + f * A.fs - g : nullptr;
     }
     P.b = A.b - g;
-    return launch_split(A, P, sgn_stage_kernel<MODE, KIND, true>, sgn_stage_kernel<MODE, KIND, false>, bytes, WX, 1,
-                        0, st);
+    constexpr int T0 = KIND == 2 ? 1 : 0, T2 = KIND == 2 ? 1 : 2;  // KIND 2: one instance
+    return launch_planned<KIND>(A, P, sgn_stage_kernel<MODE, KIND, T0>, sgn_stage_kernel<MODE, KIND, 1>,
+                                sgn_stage_kernel<MODE, KIND, T2>, opted, bytes, WX, 1, 0, st);
 }
 
 template <int KIND, bool ADAPT>
 static cudaError_t launch_s12_k(const StageArgs& A, const KPtrs& P, cudaStream_t st) {
     constexpr size_t bytes = sizeof(double2) * 2 * 3 * NPF * BX;
-    static unsigned long long opted_in = 0, opted_ed = 0;
-    cudaError_t e = smem_opt_in(opted_in, sgn_s12_kernel<KIND, ADAPT, true>, bytes);
-    if (e == cudaSuccess) e = smem_opt_in(opted_ed, sgn_s12_kernel<KIND, ADAPT, false>, bytes);
-    if (e != cudaSuccess) return e;
-    return launch_split(A, P, sgn_s12_kernel<KIND, ADAPT, true>, sgn_s12_kernel<KIND, ADAPT, false>, bytes, WX2, 2,
-                        1, st);
+    static unsigned long long opted[3] = {0, 0, 0};
+    constexpr int T0 = KIND == 2 ? 1 : 0, T2 = KIND == 2 ? 1 : 2;
+    return launch_planned<KIND>(A, P, sgn_s12_kernel<KIND, ADAPT, T0>, sgn_s12_kernel<KIND, ADAPT, 1>,
+                                sgn_s12_kernel<KIND, ADAPT, T2>, opted, bytes, WX2, 2, 1, st);
 }
 
 template <int KIND>
@@ -1193,17 +1233,12 @@ cudaError_t launch_stage(int mode, const StageArgs& A, cudaStream_t st) {
     return launch_kind<0>(mode, A, st);
 }
 
-// Kernel launches launch_stage() makes for these arguments (1, or 2 when
-// the tiles split into an edge and an interior launch).
-int stage_launches(int mode, const StageArgs& A) {
-    const TileSplit s = mode == MODE_S12 ? tile_split(A, WX2, 2, 1) : tile_split(A, WX, 1, 0);
-    if (s.n_edge < 0) return 1;
-    const int gx = s.ntx - s.ex_lo - s.ex_hi, gy = s.nby - s.ey_lo - s.ey_hi;
-    return (s.n_edge > 0 ? 1 : 0) + (gx > 0 && gy > 0 ? 1 : 0);
-}
+// Kernel launches launch_stage() makes for these arguments (edge and
+// interior tiles share one launch).
+int stage_launches(int, const StageArgs&) { return 1; }
 
-// Upper bound on the CTAs of one per-stage launch (edge + interior), the
-// size of the S3A error-partial array.
+// CTAs of one per-stage launch (edge + interior tiles), the size of the S3A
+// error-partial array.
 int stage_grid_blocks(const StageArgs& A) {
     return ((A.nx + WX - 1) / WX) * ((band_rows(A) + A.rows_per_block - 1) / A.rows_per_block);
 }
