@@ -44,6 +44,9 @@ constexpr int NPF = 4;      // ring pairs per row of the fused kernel (1/h carri
 
 template <int MODE>
 __host__ __device__ constexpr int npairs() { return MODE == MODE_S2 ? NPAIRS_S2 : NPAIRS; }
+#ifndef HSGN_S1_WARPS
+#define HSGN_S1_WARPS 16  // per-stage S1: 4 CTAs at <= 128 registers (r2: 1.91 -> 1.72 ms at 8192^2 against 5 CTAs with spills)
+#endif
 #ifndef HSGN_S3_WARPS
 #define HSGN_S3_WARPS 20  // resident warps per SM asked of the fixed-step stage-3 kernel
 #endif
@@ -52,7 +55,8 @@ __host__ __device__ constexpr int min_blocks() {
     // measured (r1): S2 (largest ring, 16 raw inputs) is best at 3 CTAs/SM;
     // the other stages fit 96 registers without spills and run best at 5
     // (expressed as resident warps per SM: 12 for S2, 20 for the others)
-    return (MODE == MODE_S2 ? 12 : MODE == MODE_S3A ? 16 : MODE == MODE_S3 ? HSGN_S3_WARPS : 20) / (BX / 32);
+    return (MODE == MODE_S2 ? 12 : MODE == MODE_S3A ? 16 : MODE == MODE_S3 ? HSGN_S3_WARPS : MODE == MODE_S1 ? HSGN_S1_WARPS : 20) /
+           (BX / 32);
 }
 
 // Per-field device pointers (kernel parameters live in the constant bank, so
