@@ -412,8 +412,11 @@ __device__ __forceinline__ void tendency(const StageArgs& A, const double2* S, i
     XQ L, R;
     neighbour_x(S + sl, L);
     neighbour_x(S + sr, R);
-#define DX(f) const double d##f##_x = sbp_d<KD>(cx, L.f, R.f)
-#define DY(f) const double d##f##_y = sbp_d<KD>(cy, ypr.f, ynr.f)
+    // interior tiles: the interior coefficients straight from the parameter
+    // bank (no closure row or column), not kept in registers
+    const double cxe = IN ? A.cpx : cx, cye = IN ? A.cpy : cy;
+#define DX(f) const double d##f##_x = sbp_d<KD>(cxe, L.f, R.f)
+#define DY(f) const double d##f##_y = sbp_d<KD>(cye, ypr.f, ynr.f)
     DX(h); DX(u); DX(v); DX(w); DX(e); DX(b); DX(hhb); DX(u2); DX(hu); DX(huv); DX(e2h); DX(huw);
     DY(h); DY(u); DY(v); DY(w); DY(e); DY(b); DY(hhb); DY(v2); DY(hv); DY(huv); DY(e2h); DY(hvw);
 #undef DX
@@ -880,7 +883,9 @@ __device__ __forceinline__ void s12_march(const StageArgs& A, const KPtrs& P, do
     // next stage-1 input while the others finish.  (Measured slower: a
     // second barrier set with a 4-slot ring B, 2.68 vs 2.63 ms.)
     Raw raw;
-    load_raw<MODE_S1>(P, (unsigned)map_row2(A, j0 - 2) * unx + col, raw);
+    // memory offsets of rows r and r-1 (mapped once, when row r is prefetched)
+    unsigned off_r = (unsigned)map_row2(A, j0 - 2) * unx + col, off_rm1 = 0u;
+    load_raw<MODE_S1>(P, off_r, raw);
 #pragma unroll 1
     for (int r = j0 - 2; r <= j1 + 1; ++r, ++k) {
         // ---- P1: stage-1 input of row r (raw of row r+1 loaded right after)
@@ -890,13 +895,17 @@ __device__ __forceinline__ void s12_march(const StageArgs& A, const KPtrs& P, do
             const bool ok = products<MODE_S1, KIND, false>(A, raw, pc + tid, ya, gd, &rhac);
             if (G.fb && r >= j0 && r < j1 && !ok) atomicAdd(&acc.bad[0], 1u);
         }
-        if (r + 1 <= j1 + 1) load_raw<MODE_S1>(P, (unsigned)map_row2(A, r + 1) * unx + col, raw);
+        unsigned off_rp1 = 0u;
+        if (r + 1 <= j1 + 1) {
+            off_rp1 = (unsigned)map_row2(A, r + 1) * unx + col;
+            load_raw<MODE_S1>(P, off_rp1, raw);
+        }
         // H1's own-column inputs need no barrier: they are requested before
         // the wait (this thread loaded them one row ago: L1/L2 hits)
         const bool do1 = r - 1 >= j0 - 1 && G.fa;
         double yj[5], kj[5];
         if (do1) {
-            const unsigned offj = (unsigned)map_row2(A, r - 1) * unx + col;
+            const unsigned offj = off_rm1;
 #pragma unroll
             for (int f = 0; f < 5; ++f) {
                 yj[f] = __ldg(P.y[f] + offj);
@@ -970,6 +979,8 @@ __device__ __forceinline__ void s12_march(const StageArgs& A, const KPtrs& P, do
         qc = t;
         rhap = rhac;
         rhbp = rhbc;
+        off_rm1 = off_r;
+        off_r = off_rp1;
 #pragma unroll
         for (int f = 0; f < 5; ++f) partp[f] = partc[f];
     }

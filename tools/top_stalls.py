@@ -18,3 +18,13 @@ for k in order[:n]:
     print(f"{100 * int(r[ist]) / tot:5.1f}%  {r[ia][-5:]}  {r[isrc].strip()}   (exec {r[iex]})")
     for c in range(max(0, k - ctx), k):
         print(f"        {body[c][ia][-5:]}  {body[c][isrc].strip()}")
+
+
+def reasons(path, addr_suffix):
+    """Per-reason stall samples of one instruction (address suffix)."""
+    rows = list(csv.reader(open(path)))
+    hdr = rows[1]
+    cols = [i for i, h in enumerate(hdr) if h.startswith("stall_") and "Not Issued" not in h]
+    for r in rows[2:]:
+        if len(r) > cols[-1] and r[0].endswith(addr_suffix):
+            return {hdr[i][6:]: int(r[i] or 0) for i in cols if int(r[i] or 0)}
