@@ -28,6 +28,7 @@ namespace hsgn_dev {
 // sgn_stage.cu
 cudaError_t launch_stage(int mode, const StageArgs& A, cudaStream_t st);
 int stage_launches(int mode, const StageArgs& A);
+cudaError_t launch_src_factors(double x0, double dx, int n, double* out, cudaStream_t st);
 int stage_grid_blocks(const StageArgs& A);
 cudaError_t launch_sum_partials(const double* part, int n, double* out, cudaStream_t st);
 // sgn_aux.cu
@@ -141,6 +142,8 @@ struct hsgn_ctx {
     int ring1 = 0;         // 1-slab ring: NCCL attached to a 1-rank periodic-y context (halos to itself)
     int b_lit = 0;         // some b value (of any slab) outside the magnitude guard (sgn_device.cuh)
     int* d_hint = nullptr; // literal-pass tile hints (StageArgs::hint_s12 / hint_stage)
+    double* d_srcx = nullptr;  // manufactured-source factor tables (StageArgs::srcx / srcy)
+    double* d_srcy = nullptr;
     long long hint_cap = 0;
     int fused = 3;         // fixed-step structure: 0 one kernel per stage, 3 S12 + S3
     int64_t n_evals = 0;
@@ -339,6 +342,10 @@ static hsgn_status setup_ctx(hsgn_ctx* c) {
     A.dx = c->dx;
     A.dy = c->dy;
     A.j_global0 = c->j_begin;
+    A.ny_global = g.ny;
+    A.y_bounded = g.kind_y == HSGN_BOUNDED;
+    A.srcx = c->d_srcx;
+    A.srcy = c->d_srcy;
     A.b = c->b;
     A.h_floor = c->phys.h_floor;
     // default launch shape: rows per CTA so that the grid is >= ~6 waves
@@ -580,8 +587,10 @@ static hsgn_status enqueue_stage(hsgn_ctx* c, int stage, const hsgn_state* y, co
 // Rows [band0, band1) of the slab only (band1 == 0: all rows).
 static hsgn_status enqueue_s12(hsgn_ctx* c, const hsgn_state* y, const hsgn_state* k1, hsgn_state* ynew,
                                StepRec* rec, const StepRec* prev, double dt, hsgn_state* part = nullptr,
-                               int band0 = 0, int band1 = 0) {
-    StageArgs A = stage_args(c, MODE_S12, 0.0);
+                               int band0 = 0, int band1 = 0, double t = 0.0) {
+    // stage times of the source term (time_integration.hpp:279,281)
+    StageArgs A = stage_args(c, MODE_S12, t + 0.5 * dt);
+    A.t2 = t + 0.75 * dt;
     A.band0 = band0;
     A.band1 = band1;
     A.a = 0.5 * dt;
@@ -613,8 +622,8 @@ static hsgn_status enqueue_s12(hsgn_ctx* c, const hsgn_state* y, const hsgn_stat
 }
 
 static hsgn_status enqueue_s3_fixed(hsgn_ctx* c, const hsgn_state* ynew, hsgn_state* k4, StepRec* rec, double dt,
-                                    int band0 = 0, int band1 = 0) {
-    StageArgs A = stage_args(c, MODE_S3, dt);  // k4 = f(ynew), FSAL
+                                    int band0 = 0, int band1 = 0, double t = 0.0) {
+    StageArgs A = stage_args(c, MODE_S3, t + dt);  // k4 = f(t + dt, ynew), FSAL
     A.band0 = band0;
     A.band1 = band1;
     A.y = ynew->base;
@@ -652,25 +661,25 @@ static Bufs ws_bufs(hsgn_ctx* c) { return Bufs{{&c->ws[0], &c->ws[1]}, {&c->ws[2
 // the S12 edge bands and those of k4 by the S3 edge bands, so the interior
 // launches never touch a row in flight.
 static hsgn_status enqueue_slab_step(hsgn_ctx* c, const Bufs& B, int p, StepRec* rec, const StepRec* prev,
-                                     double dt) {
+                                     double dt, double t) {
     const int ny = c->ny_loc, G = GHOST;
     hsgn_state *y = B.Y[p], *k1 = B.K[p], *yn = B.Y[p ^ 1], *k4 = B.K[p ^ 1];
     hsgn_status st;
     if (prev) CKE(cudaStreamWaitEvent(c->stream, c->ev_d, 0));
-    if ((st = enqueue_s12(c, y, k1, yn, rec, prev, dt, nullptr, 0, G))) return st;
-    if ((st = enqueue_s12(c, y, k1, yn, rec, prev, dt, nullptr, ny - G, ny))) return st;
+    if ((st = enqueue_s12(c, y, k1, yn, rec, prev, dt, nullptr, 0, G, t))) return st;
+    if ((st = enqueue_s12(c, y, k1, yn, rec, prev, dt, nullptr, ny - G, ny, t))) return st;
     CKE(cudaEventRecord(c->ev_a, c->stream));
     CKE(cudaStreamWaitEvent(c->cstream, c->ev_a, 0));
     if ((st = exchange_on(c, yn, 5, c->cstream))) return st;
     CKE(cudaEventRecord(c->ev_b, c->cstream));
-    if ((st = enqueue_s12(c, y, k1, yn, rec, prev, dt, nullptr, G, ny - G))) return st;
+    if ((st = enqueue_s12(c, y, k1, yn, rec, prev, dt, nullptr, G, ny - G, t))) return st;
     CKE(cudaStreamWaitEvent(c->stream, c->ev_b, 0));
-    if ((st = enqueue_s3_fixed(c, yn, k4, rec, dt, 0, G))) return st;
-    if ((st = enqueue_s3_fixed(c, yn, k4, rec, dt, ny - G, ny))) return st;
+    if ((st = enqueue_s3_fixed(c, yn, k4, rec, dt, 0, G, t))) return st;
+    if ((st = enqueue_s3_fixed(c, yn, k4, rec, dt, ny - G, ny, t))) return st;
     CKE(cudaEventRecord(c->ev_c, c->stream));
     CKE(cudaStreamWaitEvent(c->cstream, c->ev_c, 0));
     if ((st = exchange_on(c, k4, 5, c->cstream))) return st;
-    if ((st = enqueue_s3_fixed(c, yn, k4, rec, dt, G, ny - G))) return st;
+    if ((st = enqueue_s3_fixed(c, yn, k4, rec, dt, G, ny - G, t))) return st;
     CKE(cudaEventRecord(c->ev_e, c->stream));
     CKE(cudaStreamWaitEvent(c->cstream, c->ev_e, 0));
     if ((st = agree_rec(c, rec, c->cstream))) return st;  // all stage counters of this step are final
@@ -683,9 +692,10 @@ static bool slab_overlap(const hsgn_ctx* c) { return !whole(c) && !c->in_group &
 // A chunk of `steps` fixed steps as S12 + S3 per step (+1 gauge gather per
 // step with a recorder).  Whole grid: two launches per step.  NCCL slab:
 // the overlapped schedule above, or (thin slabs) the exchanges serialised
-// after each kernel.
+// after each kernel.  t: time of the first step (source terms only: a chunk
+// with a source is launched directly, not captured).
 static hsgn_status enqueue_chunk_s12(hsgn_ctx* c, const Bufs& B, int parity, int steps, double dt,
-                                     const hsgn_recorder* R) {
+                                     const hsgn_recorder* R, double t = 0.0) {
     const bool gauges = R && !R->gi.empty();
     const bool overlap = slab_overlap(c);
     hsgn_status st;
@@ -693,19 +703,21 @@ static hsgn_status enqueue_chunk_s12(hsgn_ctx* c, const Bufs& B, int parity, int
         const int p = (parity + s) & 1;
         StepRec* rec = &c->d_rec[s];
         const StepRec* prev = s ? &c->d_rec[s - 1] : nullptr;
+        const double ts = t;
+        t = t + dt;  // time_integration.hpp:321
         if (overlap) {
-            if ((st = enqueue_slab_step(c, B, p, rec, prev, dt))) return st;
+            if ((st = enqueue_slab_step(c, B, p, rec, prev, dt, ts))) return st;
             continue;
         }
         const bool kt = c->ktiming && whole(c);
         // (event record NODES of the captured graph: cudaEventRecordExternal)
         if (kt) CKE(cudaEventRecordWithFlags(c->kev[3 * s], c->stream, cudaEventRecordExternal));
-        if ((st = enqueue_s12(c, B.Y[p], B.K[p], B.Y[p ^ 1], rec, prev, dt))) return st;
+        if ((st = enqueue_s12(c, B.Y[p], B.K[p], B.Y[p ^ 1], rec, prev, dt, nullptr, 0, 0, ts))) return st;
         if (kt) CKE(cudaEventRecordWithFlags(c->kev[3 * s + 1], c->stream, cudaEventRecordExternal));
         if ((st = exchange(c, B.Y[p ^ 1], 5))) return st;
         if (gauges && (st = gauges_launch(c, B.Y[p ^ 1], R, s))) return st;
         if (kt) CKE(cudaEventRecordWithFlags(c->kev[3 * s + 2], c->stream, cudaEventRecordExternal));
-        if ((st = enqueue_s3_fixed(c, B.Y[p ^ 1], B.K[p ^ 1], rec, dt))) return st;
+        if ((st = enqueue_s3_fixed(c, B.Y[p ^ 1], B.K[p ^ 1], rec, dt, 0, 0, ts))) return st;
         if (kt && s + 1 == steps) CKE(cudaEventRecordWithFlags(c->kev[3 * steps], c->stream, cudaEventRecordExternal));
         if ((st = exchange(c, B.K[p ^ 1], 5))) return st;
         if ((st = agree_rec(c, rec))) return st;  // the next S12 halts on the global record
@@ -981,6 +993,8 @@ hsgn_status hsgn_ctx_destroy(hsgn_ctx* c) {
     if (c->d_err_part) cudaFree(c->d_err_part);
     if (c->d_scalar) cudaFree(c->d_scalar);
     if (c->d_hint) cudaFree(c->d_hint);
+    if (c->d_srcx) cudaFree(c->d_srcx);
+    if (c->d_srcy) cudaFree(c->d_srcy);
     if (c->d_rows) cudaFree(c->d_rows);
     if (c->h_rows) cudaFreeHost(c->h_rows);
     if (c->ev0) cudaEventDestroy(c->ev0);
@@ -999,6 +1013,17 @@ const char* hsgn_last_error(const hsgn_ctx* c) { return c ? c->err.c_str() : "nu
 
 hsgn_status hsgn_set_source(hsgn_ctx* c, int32_t kind) {
     if (!c || kind < 0 || kind > 1) return HSGN_EINVAL;
+    if (kind == 1 && !c->d_srcx) {  // the per-column / per-row factors of the source term, once
+        DeviceGuard dg_(c->device);
+        const hsgn_grid& g = c->grid;
+        CK(cudaMalloc(&c->d_srcx, sizeof(double) * 4 * g.nx));
+        CK(cudaMalloc(&c->d_srcy, sizeof(double) * 4 * g.ny));
+        CK(launch_src_factors(g.x_min, c->dx, g.nx, c->d_srcx, c->stream));
+        CK(launch_src_factors(g.y_min, c->dy, g.ny, c->d_srcy, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        c->base.srcx = c->d_srcx;
+        c->base.srcy = c->d_srcy;
+    }
     c->source = kind;
     return HSGN_OK;
 }
@@ -1201,7 +1226,7 @@ uint64_t bits_of(double v) {
 hsgn_status enqueue_chunk(hsgn_ctx* c, const Bufs& B, int parity, int steps, double t, double dt,
                           const hsgn_recorder* R) {
     reset_recs(c, steps);
-    if (c->fused == 3 && c->source == 0) return enqueue_chunk_s12(c, B, parity, steps, dt, R);
+    if (c->fused == 3) return enqueue_chunk_s12(c, B, parity, steps, dt, R, t);
     return enqueue_chunk_stages(c, B, parity, steps, t, dt, R);
 }
 
@@ -1595,8 +1620,9 @@ extern "C" hsgn_status hsgn_solve_recorded(hsgn_ctx* c, const hsgn_state* q0, do
         // ---- one attempt (adaptive, clipped or observed step)
         const int q = p ^ 1;
         reset_recs(c, 1);
-        if (c->fused == 3 && c->source == 0) {  // S12 + S3 (with error partials when adaptive)
-            st = enqueue_s12(c, B.Y[p], B.K[p], B.Y[q], &c->d_rec[0], nullptr, dt, fixed ? nullptr : &c->ws[5]);
+        if (c->fused == 3) {  // S12 + S3 (with error partials when adaptive)
+            st = enqueue_s12(c, B.Y[p], B.K[p], B.Y[q], &c->d_rec[0], nullptr, dt, fixed ? nullptr : &c->ws[5], 0, 0,
+                             t);
             if (!st) st = exchange(c, B.Y[q], 5);
             if (!st)
                 st = enqueue_stage(c, 3, B.Y[p], B.K[p], &c->ws[4], B.Y[q], B.K[q], &c->ws[5], &c->d_rec[0], nullptr, t,

@@ -267,4 +267,26 @@ cudaError_t launch_init_aux(const AuxArgs& A, double* q, cudaStream_t st) {
     return cudaGetLastError();
 }
 
+// Factors of the manufactured source term along one grid direction:
+// (sin 2pi x, cos 2pi x, sin 4pi x, cos 4pi x) at x = x0 + i dx
+// (Grid2D::x, grid.hpp:24-25), read by sgn_stage.cu mms_source.
+__global__ void src_factor_kernel(double x0, double dx, int n, double* out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double tp = 2.0 * 3.14159265358979323846, fp = 4.0 * 3.14159265358979323846;
+    const double x = dadd(x0, dmul((double)i, dx));
+    double s1, c1, s2, c2;
+    sincos(tp * x, &s1, &c1);
+    sincos(fp * x, &s2, &c2);
+    out[4 * i] = s1;
+    out[4 * i + 1] = c1;
+    out[4 * i + 2] = s2;
+    out[4 * i + 3] = c2;
+}
+
+cudaError_t launch_src_factors(double x0, double dx, int n, double* out, cudaStream_t st) {
+    src_factor_kernel<<<(n + 255) / 256, 256, 0, st>>>(x0, dx, n, out);
+    return cudaGetLastError();
+}
+
 }  // namespace hsgn_dev

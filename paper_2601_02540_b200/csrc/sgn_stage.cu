@@ -208,15 +208,20 @@ __device__ __forceinline__ bool products(const StageArgs& A, const Raw& raw, dou
 }
 
 // Manufactured source terms S(t, x, y) (scenarios.hpp:179-217 forcing; the
-// closed form restated in DESIGN.md section 5 and oracle/hsgn_oracle.c).
-__device__ __noinline__ void mms_source(double t, double x, double y, double g, double* s) {
+// closed form restated in DESIGN.md section 5 and oracle/hsgn_oracle.c),
+// from precomputed factors: xf = (sin 2pi x, cos 2pi x, sin 4pi x, cos 4pi x)
+// of the node's column (srcx table), yf the same of its row (srcy table),
+// tsc = (sin 2pi t, cos 2pi t) of the stage time (shared memory, once per
+// launch).  The tables hold the grid's own nodes, so a halo row / column of
+// a tile takes the factors of the row / column it wraps to.
+struct Src5 {
+    double v[5];
+};
+__device__ __noinline__ Src5 mms_source(const double* xf, const double* yf, const double* tsc, double g) {
     const double tp = 2.0 * 3.14159265358979323846, fp = 4.0 * 3.14159265358979323846;
-    double s1x, c1x, s1y, c1y, s2x, c2x, s2y, c2y, st, ct;
-    sincos(tp * x, &s1x, &c1x);
-    sincos(tp * y, &s1y, &c1y);
-    sincos(fp * x, &s2x, &c2x);
-    sincos(fp * y, &s2y, &c2y);
-    sincos(tp * t, &st, &ct);
+    const double s1x = xf[0], c1x = xf[1], s2x = xf[2], c2x = xf[3];
+    const double s1y = yf[0], c1y = yf[1], s2y = yf[2], c2y = yf[3];
+    const double st = tsc[0], ct = tsc[1];
     const double bx = -(2.0 / 25.0) * tp * s1x * c1y - (1.0 / 25.0) * fp * s2x * c2y;
     const double by = -(2.0 / 25.0) * tp * c1x * s1y - (1.0 / 25.0) * fp * c2x * s2y;
     const double bxx = -(2.0 / 25.0) * tp * tp * c1x * c1y - (1.0 / 25.0) * fp * fp * c2x * c2y;
@@ -239,11 +244,18 @@ __device__ __noinline__ void mms_source(double t, double x, double y, double g, 
     const double wy = -hy * D - h * vyy + 1.5 * Gy;
     const double wt = -ht * D - h * Dt + 1.5 * Gt;
     const double sh = ht + (hx * u + h * ux) + (hy * v + h * vy);
-    s[0] = sh;
-    s[1] = ut + u * ux + g * (hx + bx);
-    s[2] = vt + v * vy + g * (hy + by);
-    s[3] = wt + u * wx + v * wy;
-    s[4] = sh;
+    Src5 s;  // returned in registers (an output array would go through local memory)
+    s.v[0] = sh;
+    s.v[1] = ut + u * ux + g * (hx + bx);
+    s.v[2] = vt + v * vy + g * (hy + by);
+    s.v[3] = wt + u * wx + v * wy;
+    s.v[4] = sh;
+    return s;
+}
+
+// (sin 2pi t, cos 2pi t) of a stage time into shared memory (one thread).
+__device__ __forceinline__ void stage_time_factors(double t, double* tsc) {
+    sincos(2.0 * 3.14159265358979323846 * t, &tsc[0], &tsc[1]);
 }
 
 // Adaptive-mode epilogue, kept out of line so it does not raise the register
@@ -331,6 +343,7 @@ struct Thr {
     double my_err;
     Guard gd;           // fast pass: magnitude guard over the stage inputs this thread formed
     int t0;             // split-barrier step index of this pass's prologue
+    const double* tsc;  // shared (sin, cos)(2 pi t) of the stage time (sources)
 };
 
 // x-quantities of a neighbour column re-formed from its ring pairs, with the
@@ -400,7 +413,7 @@ __device__ __forceinline__ void neighbour_y(const double2* S, YQ& Y) {
 template <int KIND, bool SW, bool SRC, bool IN, bool LIT>
 __device__ __forceinline__ void tendency(const StageArgs& A, const double2* S, int tid, int sl, int sr, double cx,
                                          double cy, bool xl, bool xr, int i, int j, const YQ& ypr, const YQ& ynr,
-                                         double rh, double o[5]) {
+                                         double rh, double o[5], const double* tsc = nullptr) {
     constexpr int KD = (LIT && KIND == 2) ? 1 : KIND;  // derivative form
     constexpr bool CF = KD == 2;                       // common factor applied once per tendency
     const double2* Sc = S + tid;  // row j, own column
@@ -525,12 +538,15 @@ __device__ __forceinline__ void tendency(const StageArgs& A, const double2* S, i
         o[4] = 0.0;
     }
     if (SRC && A.source) {  // add_manufactured_sources: after assembly (rhs.hpp:212-213)
-        const double xg = dadd(A.x_min, dmul((double)i, A.dx));
-        const double yg = dadd(A.y_min, dmul((double)(A.j_global0 + j), A.dy));
-        double s5[5];
-        mms_source(A.t, xg, yg, A.g, s5);
+        // the node's grid column / global row (halo nodes wrap or clamp like the grid)
+        int ig = i, jg = A.j_global0 + j;
+        if (ig < 0) ig = A.x_bounded ? 0 : ig + A.nx;
+        if (ig >= A.nx) ig = A.x_bounded ? A.nx - 1 : ig - A.nx;
+        if (jg < 0) jg = A.y_bounded ? 0 : jg + A.ny_global;
+        if (jg >= A.ny_global) jg = A.y_bounded ? A.ny_global - 1 : jg - A.ny_global;
+        const Src5 s5 = mms_source(A.srcx + 4 * ig, A.srcy + 4 * jg, tsc, A.g);
 #pragma unroll
-        for (int f = 0; f < 5; ++f) o[f] = dadd(o[f], s5[f]);
+        for (int f = 0; f < 5; ++f) o[f] = dadd(o[f], s5.v[f]);
     }
 }
 
@@ -599,7 +615,7 @@ __device__ __forceinline__ void march_row(const StageArgs& A, const KPtrs& P, Th
     }
     double o[5];
     tendency<KIND, true, true, IN, LIT>(A, S, T.tid, T.sl, T.sr, T.cx, cy, T.xl, T.xr, T.i, j, ypr, yn,
-                                        Sc[P_RH * BX].x, o);
+                                        Sc[P_RH * BX].x, o, T.tsc);
     // ---- epilogue
     if (MODE == MODE_S2) {
         const double2 y01 = Sc[P_YP01 * BX], y23 = Sc[P_YP23 * BX], y4 = Sc[P_YP4 * BX];
@@ -698,13 +714,15 @@ __device__ __forceinline__ void march_tile(const StageArgs& A, const KPtrs& P, T
 
 template <int MODE, int KIND, bool IN>
 __device__ __forceinline__ void stage_body(const StageArgs& A, const KPtrs& P, double2* ring, unsigned long long* s_min,
-                                           double* s_err, unsigned long long* sbar) {
+                                           double* s_err, unsigned long long* sbar, double* s_tsc) {
     const int tid = threadIdx.x;
     Thr T;
     T.bad = 0;
     T.my_min = ~0ull;
     T.my_err = 0.0;
     T.t0 = 0;
+    T.tsc = s_tsc;
+    if (A.source && tid == 0) stage_time_factors(A.t, s_tsc);  // read after the first row barrier
 
     if (split_bar<MODE>()) {
         if (tid == 0) {
@@ -768,12 +786,13 @@ __global__ void __launch_bounds__(BX, min_blocks<MODE>()) sgn_stage_kernel(const
     __shared__ unsigned long long s_min[BX / 32];
     __shared__ double s_err[BX / 32];
     __shared__ __align__(8) unsigned long long sbar[2];
+    __shared__ double s_tsc[2];
     __shared__ int s_skip;
     if (halted(A, &s_skip)) return;
     if (TILES == 1 || (TILES == 2 && !edge_cta(A)))
-        stage_body<MODE, KIND, true>(A, P, ring, s_min, s_err, sbar);
+        stage_body<MODE, KIND, true>(A, P, ring, s_min, s_err, sbar, s_tsc);
     else
-        stage_body<MODE, KIND, false>(A, P, ring, s_min, s_err, sbar);
+        stage_body<MODE, KIND, false>(A, P, ring, s_min, s_err, sbar, s_tsc);
 }
 
 // Fused kernels: memory row of -GHOST <= jr < ny + GHOST, counted from row
@@ -859,9 +878,9 @@ __device__ __forceinline__ S12Geo s12_geo(const StageArgs& A) {
 // ADAPT: also store the error partial ((d1 k1 + d2 k2) + d3 k3)
 // (time_integration.hpp:128-129, the S2 epilogue of the per-stage path) for
 // the adaptive S3's error norm.
-template <int KIND, bool ADAPT, bool IN, bool LIT>
+template <int KIND, bool ADAPT, bool SRC, bool IN, bool LIT>
 __device__ __forceinline__ void s12_march(const StageArgs& A, const KPtrs& P, double2* ring,
-                                          unsigned long long* s_bar, int& k, S12Acc& acc) {
+                                          unsigned long long* s_bar, int& k, S12Acc& acc, const double* s_tsc) {
     const S12Geo G = s12_geo<KIND, IN>(A);
     const int tid = G.tid, i = G.i, j0 = G.j0, j1 = G.j1, ny = A.ny;
     const unsigned unx = (unsigned)A.nx, col = G.col;
@@ -924,8 +943,8 @@ __device__ __forceinline__ void s12_march(const StageArgs& A, const KPtrs& P, do
             if (hi) neighbour_y(pb + tid, yc);
             const double cy = (j == G.jc0 || j == G.jc1) ? A.c1y : A.cpy;
             double k2[5];
-            tendency<KIND, false, false, IN, LIT>(A, pb, tid, G.sl, G.sr, G.cx, cy, G.xl, G.xr, i, j, yp,
-                                                  hi ? yc : ya, rhap, k2);
+            tendency<KIND, false, SRC, IN, LIT>(A, pb, tid, G.sl, G.sr, G.cx, cy, G.xl, G.xr, i, j, yp,
+                                                hi ? yc : ya, rhap, k2, s_tsc);
             double q[5];
 #pragma unroll
             for (int f = 0; f < 5; ++f) {
@@ -955,8 +974,8 @@ __device__ __forceinline__ void s12_march(const StageArgs& A, const KPtrs& P, do
                 for (int f = 0; f < 5; ++f) e12[f] = P.part[f][off];
             }
             double k3[5];
-            tendency<KIND, false, false, IN, LIT>(A, qb, tid, G.sl, G.sr, G.cx, cy, G.xl, G.xr, i, j, yp,
-                                                  hi ? yc : yb, rhbp, k3);
+            tendency<KIND, false, SRC, IN, LIT>(A, qb, tid, G.sl, G.sr, G.cx, cy, G.xl, G.xr, i, j, yp,
+                                                hi ? yc : yb, rhbp, k3, s_tsc + 2);
 #pragma unroll
             for (int f = 0; f < 5; ++f) P.out[f][off] = dadd(partp[f], dmul(A.c3, k3[f]));  // state_add3
             if (ADAPT) {  // ((d1 k1 + d2 k2) + d3 k3) (time_integration.hpp:128-129)
@@ -987,7 +1006,7 @@ __device__ __forceinline__ void s12_march(const StageArgs& A, const KPtrs& P, do
     acc.any = guard_fail(gd);
 }
 
-template <int KIND, bool ADAPT, bool IN>
+template <int KIND, bool ADAPT, bool SRC, bool IN>
 __device__ __forceinline__ void s12_body(const StageArgs& A, const KPtrs& P, double2* ring, unsigned long long* s_min,
                                          unsigned long long* s_bar) {
     const int tid = threadIdx.x;
@@ -997,7 +1016,12 @@ __device__ __forceinline__ void s12_body(const StageArgs& A, const KPtrs& P, dou
     }
     __syncthreads();
     __shared__ unsigned s_bad[2];
+    __shared__ double s_tsc[4];  // SRC: (sin, cos)(2 pi t) of the stage-1 and stage-2 times
     if (tid < 2) s_bad[tid] = 0u;
+    if (SRC && tid == 0) {
+        stage_time_factors(A.t, s_tsc);
+        stage_time_factors(A.t2, s_tsc + 2);
+    }
     __syncthreads();
     S12Acc acc{s_bad, ~0ull, false};
     int k = 0;
@@ -1006,7 +1030,7 @@ __device__ __forceinline__ void s12_body(const StageArgs& A, const KPtrs& P, dou
     const bool hinted = !A.lit_all && hint && *hint;
     bool redo = A.lit_all || hinted;
     if (!redo) {
-        s12_march<KIND, ADAPT, IN, false>(A, P, ring, s_bar, k, acc);
+        s12_march<KIND, ADAPT, SRC, IN, false>(A, P, ring, s_bar, k, acc, s_tsc);
         redo = __syncthreads_or(acc.any);
         if (redo) {  // the fast pass's counts are discarded
             if (tid < 2) s_bad[tid] = 0u;
@@ -1016,7 +1040,7 @@ __device__ __forceinline__ void s12_body(const StageArgs& A, const KPtrs& P, dou
     bool need = false;
     if (redo) {  // literal pass (outputs, counters and min replaced)
         acc = S12Acc{s_bad, ~0ull, false};
-        s12_march<KIND, ADAPT, IN, true>(A, P, ring, s_bar, k, acc);
+        s12_march<KIND, ADAPT, SRC, IN, true>(A, P, ring, s_bar, k, acc, s_tsc);
         if (hint) need = __syncthreads_or(acc.any);
     }
     if (hint && tid == 0 && need != hinted) *hint = need;
@@ -1035,7 +1059,7 @@ __device__ __forceinline__ void s12_body(const StageArgs& A, const KPtrs& P, dou
     }
 }
 
-template <int KIND, bool ADAPT, int TILES>
+template <int KIND, bool ADAPT, bool SRC, int TILES>
 __global__ void __launch_bounds__(BX, HSGN_S12_MINB) sgn_s12_kernel(const StageArgs A, const KPtrs P) {
     extern __shared__ __align__(16) double2 ring[];  // ring A | ring B, each 3 x NPF x BX
     __shared__ unsigned long long s_min[BX / 32];
@@ -1043,9 +1067,9 @@ __global__ void __launch_bounds__(BX, HSGN_S12_MINB) sgn_s12_kernel(const StageA
     __shared__ int s_skip;
     if (halted(A, &s_skip)) return;
     if (TILES == 1 || (TILES == 2 && !edge_cta(A)))
-        s12_body<KIND, ADAPT, true>(A, P, ring, s_min, s_bar);
+        s12_body<KIND, ADAPT, SRC, true>(A, P, ring, s_min, s_bar);
     else
-        s12_body<KIND, ADAPT, false>(A, P, ring, s_min, s_bar);
+        s12_body<KIND, ADAPT, SRC, false>(A, P, ring, s_min, s_bar);
 }
 
 // Deterministic final sum of per-block partials (single CTA, fixed order,
@@ -1205,18 +1229,18 @@ static cudaError_t launch_mode(const StageArgs& A, cudaStream_t st) {
                                 sgn_stage_kernel<MODE, KIND, T2>, opted, bytes, WX, 1, 0, st);
 }
 
-template <int KIND, bool ADAPT>
+template <int KIND, bool ADAPT, bool SRC>
 static cudaError_t launch_s12_k(const StageArgs& A, const KPtrs& P, cudaStream_t st) {
     constexpr size_t bytes = sizeof(double2) * 2 * 3 * NPF * BX;
     static unsigned long long opted[3] = {0, 0, 0};
     constexpr int T0 = KIND == 2 ? 1 : 0, T2 = KIND == 2 ? 1 : 2;
-    return launch_planned<KIND>(A, P, sgn_s12_kernel<KIND, ADAPT, T0>, sgn_s12_kernel<KIND, ADAPT, 1>,
-                                sgn_s12_kernel<KIND, ADAPT, T2>, opted, bytes, WX2, 2, 1, st);
+    return launch_planned<KIND>(A, P, sgn_s12_kernel<KIND, ADAPT, SRC, T0>, sgn_s12_kernel<KIND, ADAPT, SRC, 1>,
+                                sgn_s12_kernel<KIND, ADAPT, SRC, T2>, opted, bytes, WX2, 2, 1, st);
 }
 
 template <int KIND>
 static cudaError_t launch_s12(const StageArgs& A, cudaStream_t st) {
-    if (A.source || A.shallow) return cudaErrorInvalidValue;  // fused kernels: neither (see tendency)
+    if (A.shallow) return cudaErrorInvalidValue;  // rhs_shallow_water: per-stage kernels only
     KPtrs P;
     const long long g = A.nx;
     for (int f = 0; f < 5; ++f) {
@@ -1227,7 +1251,9 @@ static cudaError_t launch_s12(const StageArgs& A, cudaStream_t st) {
         P.out[f] = A.out + f * A.fs - GHOST * g;
     }
     P.b = A.b - GHOST * g;
-    return A.adaptive ? launch_s12_k<KIND, true>(A, P, st) : launch_s12_k<KIND, false>(A, P, st);
+    if (A.source)
+        return A.adaptive ? launch_s12_k<KIND, true, true>(A, P, st) : launch_s12_k<KIND, false, true>(A, P, st);
+    return A.adaptive ? launch_s12_k<KIND, true, false>(A, P, st) : launch_s12_k<KIND, false, false>(A, P, st);
 }
 
 template <int KIND>
