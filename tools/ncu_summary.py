@@ -1,5 +1,5 @@
 """Summarise an ncu report (--set full) into the metrics the roofline needs.
-Usage: ncu_summary.py report.ncu-rep [points_per_launch]"""
+Usage: ncu_summary.py report.ncu-rep|raw.csv [points_per_launch]"""
 import csv
 import io
 import json
@@ -8,7 +8,9 @@ import sys
 
 rep = sys.argv[1]
 pts = float(sys.argv[2]) if len(sys.argv) > 2 else 8192 * 8192
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+# a report, or its `--page raw --csv` export
+raw = open(rep).read() if rep.endswith(".csv") else \
+    subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
 hdr = rows[0]
 keys = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
