@@ -217,7 +217,7 @@ __device__ __forceinline__ bool products(const StageArgs& A, const Raw& raw, dou
 struct Src5 {
     double v[5];
 };
-__device__ __noinline__ Src5 mms_source(const double* xf, const double* yf, const double* tsc, double g) {
+static __device__ __noinline__ Src5 mms_source(const double* xf, const double* yf, const double* tsc, double g) {
     const double tp = 2.0 * 3.14159265358979323846, fp = 4.0 * 3.14159265358979323846;
     const double s1x = xf[0], c1x = xf[1], s2x = xf[2], c2x = xf[3];
     const double s1y = yf[0], c1y = yf[1], s2y = yf[2], c2y = yf[3];
@@ -263,7 +263,7 @@ __device__ __forceinline__ void stage_time_factors(double t, double* tsc) {
 // by value: taking the address of the kernel-parameter structs would copy
 // them to local memory.)
 // S2: ((d1 k1 + d2 k2) + d3 k3) (time_integration.hpp:128-129, first 3 terms)
-__device__ __noinline__ void s2_error_partial(const double* kc, const double* k, double* part, long long fs,
+static __device__ __noinline__ void s2_error_partial(const double* kc, const double* k, double* part, long long fs,
                                               unsigned off, double d1, double d2, double d3, double o0, double o1,
                                               double o2, double o3, double o4) {
     const double o[5] = {o0, o1, o2, o3, o4};
@@ -1072,32 +1072,6 @@ __global__ void __launch_bounds__(BX, HSGN_S12_MINB) sgn_s12_kernel(const StageA
         s12_body<KIND, ADAPT, SRC, false>(A, P, ring, s_min, s_bar);
 }
 
-// Deterministic final sum of per-block partials (single CTA, fixed order,
-// compensated); result goes to out[0].
-__global__ void __launch_bounds__(256) sum_partials_kernel(const double* part, int n, double* out) {
-    __shared__ double sh[256], sc[256];
-    double s = 0.0, c = 0.0;
-    for (int k = threadIdx.x; k < n; k += 256) {  // Kahan per thread, fixed stride order
-        const double term = dsub(part[k], c);
-        const double t = dadd(s, term);
-        c = dsub(dsub(t, s), term);
-        s = t;
-    }
-    sh[threadIdx.x] = s;
-    sc[threadIdx.x] = c;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double S = 0.0, Cc = 0.0;
-        for (int k = 0; k < 256; ++k) {
-            const double term = dsub(sh[k], dadd(Cc, sc[k]));
-            const double t = dadd(S, term);
-            Cc = dsub(dsub(t, S), term);
-            S = t;
-        }
-        out[0] = S;
-    }
-}
-
 // ----------------------------------------------------------------- launch
 
 static int band_rows(const StageArgs& A) { return (A.band1 > 0 ? A.band1 : A.ny) - A.band0; }
@@ -1256,22 +1230,70 @@ static cudaError_t launch_s12(const StageArgs& A, cudaStream_t st) {
     return A.adaptive ? launch_s12_k<KIND, true, false>(A, P, st) : launch_s12_k<KIND, false, false>(A, P, st);
 }
 
-template <int KIND>
-static cudaError_t launch_kind(int mode, const StageArgs& A, cudaStream_t st) {
+// Instantiation units: build.py compiles this file once per stencil kind and
+// kernel family (-DHSGN_INST_KIND=k -DHSGN_INST_S12=0|1), so the kernel
+// instances compile in parallel; the plain compile (no HSGN_INST_KIND) holds
+// the dispatcher and the non-template kernels.
+#define HSGN_CAT2(a, b) a##b
+#define HSGN_CAT(a, b) HSGN_CAT2(a, b)
+cudaError_t launch_s12_k0(const StageArgs& A, cudaStream_t st);
+cudaError_t launch_s12_k1(const StageArgs& A, cudaStream_t st);
+cudaError_t launch_s12_k2(const StageArgs& A, cudaStream_t st);
+cudaError_t launch_mode_k0(int mode, const StageArgs& A, cudaStream_t st);
+cudaError_t launch_mode_k1(int mode, const StageArgs& A, cudaStream_t st);
+cudaError_t launch_mode_k2(int mode, const StageArgs& A, cudaStream_t st);
+
+#if defined(HSGN_INST_KIND) && HSGN_INST_S12
+cudaError_t HSGN_CAT(launch_s12_k, HSGN_INST_KIND)(const StageArgs& A, cudaStream_t st) {
+    return launch_s12<HSGN_INST_KIND>(A, st);
+}
+#elif defined(HSGN_INST_KIND)
+cudaError_t HSGN_CAT(launch_mode_k, HSGN_INST_KIND)(int mode, const StageArgs& A, cudaStream_t st) {
+    constexpr int KIND = HSGN_INST_KIND;
     switch (mode) {
-        case MODE_S12: return launch_s12<KIND>(A, st);
         case MODE_RHS: return launch_mode<MODE_RHS, KIND>(A, st);
         case MODE_S1: return launch_mode<MODE_S1, KIND>(A, st);
         case MODE_S2: return launch_mode<MODE_S2, KIND>(A, st);
         default: return A.adaptive ? launch_mode<MODE_S3A, KIND>(A, st) : launch_mode<MODE_S3, KIND>(A, st);
     }
 }
+#else
+// Deterministic final sum of per-block partials (single CTA, fixed order,
+// compensated); result goes to out[0].
+__global__ void __launch_bounds__(256) sum_partials_kernel(const double* part, int n, double* out) {
+    __shared__ double sh[256], sc[256];
+    double s = 0.0, c = 0.0;
+    for (int k = threadIdx.x; k < n; k += 256) {  // Kahan per thread, fixed stride order
+        const double term = dsub(part[k], c);
+        const double t = dadd(s, term);
+        c = dsub(dsub(t, s), term);
+        s = t;
+    }
+    sh[threadIdx.x] = s;
+    sc[threadIdx.x] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double S = 0.0, Cc = 0.0;
+        for (int k = 0; k < 256; ++k) {
+            const double term = dsub(sh[k], dadd(Cc, sc[k]));
+            const double t = dadd(S, term);
+            Cc = dsub(dsub(t, S), term);
+            S = t;
+        }
+        out[0] = S;
+    }
+}
 
 // A.pow2 carries the stencil kind chosen by the host (see sbp_d).
 cudaError_t launch_stage(int mode, const StageArgs& A, cudaStream_t st) {
-    if (A.pow2 == 2) return launch_kind<2>(mode, A, st);
-    if (A.pow2 == 1) return launch_kind<1>(mode, A, st);
-    return launch_kind<0>(mode, A, st);
+    if (mode == MODE_S12) {
+        if (A.pow2 == 2) return launch_s12_k2(A, st);
+        if (A.pow2 == 1) return launch_s12_k1(A, st);
+        return launch_s12_k0(A, st);
+    }
+    if (A.pow2 == 2) return launch_mode_k2(mode, A, st);
+    if (A.pow2 == 1) return launch_mode_k1(mode, A, st);
+    return launch_mode_k0(mode, A, st);
 }
 
 // Kernel launches launch_stage() makes for these arguments (edge and
@@ -1288,5 +1310,6 @@ cudaError_t launch_sum_partials(const double* part, int n, double* out, cudaStre
     sum_partials_kernel<<<1, 256, 0, st>>>(part, n, out);
     return cudaGetLastError();
 }
+#endif
 
 }  // namespace hsgn_dev
