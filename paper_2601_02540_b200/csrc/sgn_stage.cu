@@ -32,6 +32,7 @@
 #include <algorithm>
 #include <climits>
 #include <cstdint>
+#include <type_traits>
 
 #include "sgn_device.cuh"
 
@@ -152,7 +153,7 @@ __device__ __forceinline__ void load_raw(const KPtrs& P, unsigned off, Raw& r) {
 // (h, u, v, w, eta) and b: stores the ring pairs of the node (S already
 // offset by ring row and column), fills the y-quantities and the node's
 // magnitude guard (guard_add); returns h > 0.
-template <int KIND, bool STORE_RH = true>
+template <int KIND, bool LIT, bool STORE_RH = true>
 __device__ __forceinline__ bool products_q(const double q[5], double b, double2* S, YQ& Y, double* rh_out,
                                            Guard& gd) {
     const double h = q[0], u = q[1], v = q[2], w = q[3], e = q[4];
@@ -161,7 +162,8 @@ __device__ __forceinline__ bool products_q(const double q[5], double b, double2*
     const double rh = rcp_or_nan(h);
     bool slow = false;
     double r = div_fast(e, h, rh, slow);  // eta/h computed once (rhs.hpp:86-88)
-    if (slow) r = e / h;
+    if (LIT && slow) r = e / h;  // fast pass: deferred to the literal pass (guard_mark)
+    guard_mark(gd, slow);
     const double hpb = dadd(h, b);
     const double hv = dmul(h, v);
     S[P_HU * BX] = make_double2(h, u);
@@ -188,14 +190,14 @@ __device__ __forceinline__ bool products_q(const double q[5], double b, double2*
 // The same from raw stage data: q = y + a*k (state_add1,
 // time_integration.hpp:61-75) for S1/S2, q = y otherwise; S2 also stores
 // ((y + c1 k1) + c2 k2), the k3-free part of ynew (state_add3).
-template <int MODE, int KIND, bool STORE_RH = true>
+template <int MODE, int KIND, bool LIT, bool STORE_RH = true>
 __device__ __forceinline__ bool products(const StageArgs& A, const Raw& raw, double2* S, YQ& Y, Guard& gd,
                                          double* rh_out = nullptr) {
     double q[5];
 #pragma unroll
     for (int f = 0; f < 5; ++f)
         q[f] = (MODE == MODE_S1 || MODE == MODE_S2) ? dadd(raw.y[f], dmul(A.a, raw.k[f])) : raw.y[f];
-    const bool ok = products_q<KIND, STORE_RH>(q, raw.b, S, Y, rh_out, gd);
+    const bool ok = products_q<KIND, LIT, STORE_RH>(q, raw.b, S, Y, rh_out, gd);
     if (MODE == MODE_S2) {
         double yp[5];
 #pragma unroll
@@ -413,7 +415,7 @@ __device__ __forceinline__ void neighbour_y(const double2* S, YQ& Y) {
 template <int KIND, bool SW, bool SRC, bool IN, bool LIT>
 __device__ __forceinline__ void tendency(const StageArgs& A, const double2* S, int tid, int sl, int sr, double cx,
                                          double cy, bool xl, bool xr, int i, int j, const YQ& ypr, const YQ& ynr,
-                                         double rh, double o[5], const double* tsc = nullptr) {
+                                         double rh, double o[5], Guard& gd, const double* tsc = nullptr) {
     constexpr int KD = (LIT && KIND == 2) ? 1 : KIND;  // derivative form
     constexpr bool CF = KD == 2;                       // common factor applied once per tendency
     const double2* Sc = S + tid;  // row j, own column
@@ -519,7 +521,8 @@ __device__ __forceinline__ void tendency(const StageArgs& A, const double2* S, i
     {  // the three "/h" (rhs.hpp:175,188,200), one range test per node
         bool slow = false;
         double qu = div_fast(nu, h, rh, slow), qv = div_fast(nv, h, rh, slow), qw = div_fast(nw, h, rh, slow);
-        if (slow) {
+        guard_mark(gd, slow);  // fast pass: the literal pass redoes the tile
+        if (LIT && slow) {
             qu = nu / h;
             qv = nv / h;
             qw = nw / h;
@@ -563,7 +566,7 @@ __device__ __forceinline__ void tendency(const StageArgs& A, const double2* S, i
 // One row of the march: form row jn = j+1 (ring slot SN, register set yn),
 // then finish row j (ring slot SC; row j-1 is register set yp for S2, its
 // ring entry otherwise).
-template <int MODE, int KIND, bool IN, bool LIT, int SC>
+template <int MODE, int KIND, bool IN, bool LIT, int SC, bool SRC>
 __device__ __forceinline__ void march_row(const StageArgs& A, const KPtrs& P, Thr& T, double2* ring, int j0, int j,
                                           const YQ& yp, YQ& yn, Raw& raw, unsigned long long* sbar) {
     constexpr int NP = npairs<MODE>();
@@ -572,7 +575,7 @@ __device__ __forceinline__ void march_row(const StageArgs& A, const KPtrs& P, Th
     const int jn = j + 1;
     const unsigned nx = (unsigned)A.nx;
     {  // products of row jn (for D_y of row j, and D_x of row jn one step later)
-        const bool ok = products<MODE, KIND>(A, raw, ring + SN * (NP * BX) + T.tid, yn, T.gd);
+        const bool ok = products<MODE, KIND, LIT>(A, raw, ring + SN * (NP * BX) + T.tid, yn, T.gd);
         if (T.finish && jn < T.j1 && !ok) ++T.bad;
     }
     // register prefetch of raw(jn+1), in flight during the finish of row j
@@ -614,8 +617,8 @@ __device__ __forceinline__ void march_row(const StageArgs& A, const KPtrs& P, Th
         }
     }
     double o[5];
-    tendency<KIND, true, true, IN, LIT>(A, S, T.tid, T.sl, T.sr, T.cx, cy, T.xl, T.xr, T.i, j, ypr, yn,
-                                        Sc[P_RH * BX].x, o, T.tsc);
+    tendency<KIND, true, SRC, IN, LIT>(A, S, T.tid, T.sl, T.sr, T.cx, cy, T.xl, T.xr, T.i, j, ypr, yn,
+                                        Sc[P_RH * BX].x, o, T.gd, T.tsc);
     // ---- epilogue
     if (MODE == MODE_S2) {
         const double2 y01 = Sc[P_YP01 * BX], y23 = Sc[P_YP23 * BX], y4 = Sc[P_YP4 * BX];
@@ -682,7 +685,7 @@ __device__ __forceinline__ int tile_geo(const StageArgs& A, Thr& T) {
 }
 
 // One pass over the tile: prologue (rows j0-1, j0) and the march.
-template <int MODE, int KIND, bool IN, bool LIT>
+template <int MODE, int KIND, bool IN, bool LIT, bool SRC>
 __device__ __forceinline__ void march_tile(const StageArgs& A, const KPtrs& P, Thr& T, double2* ring,
                                            unsigned long long* sbar) {
     constexpr int NP = npairs<MODE>();
@@ -692,10 +695,10 @@ __device__ __forceinline__ void march_tile(const StageArgs& A, const KPtrs& P, T
     YQ ya, yb, yc;
     Raw raw;
     load_raw<MODE>(P, (unsigned)map_row(A, j0 - 1) * unx + T.col, raw);
-    products<MODE, KIND>(A, raw, ring + 2 * (NP * BX) + T.tid, yc, T.gd);
+    products<MODE, KIND, LIT>(A, raw, ring + 2 * (NP * BX) + T.tid, yc, T.gd);
     load_raw<MODE>(P, (unsigned)(j0 + 1) * unx + T.col, raw);
     {
-        const bool ok = products<MODE, KIND>(A, raw, ring + T.tid, ya, T.gd);
+        const bool ok = products<MODE, KIND, LIT>(A, raw, ring + T.tid, ya, T.gd);
         if (T.finish && !ok) ++T.bad;
     }
     load_raw<MODE>(P, (unsigned)map_row(A, j0 + 1) * unx + T.col, raw);
@@ -703,16 +706,16 @@ __device__ __forceinline__ void march_tile(const StageArgs& A, const KPtrs& P, T
     // ---- march, unrolled by 3: row j lives in ring slot (j-j0)%3 and register
     // set {a,b,c}[(j-j0)%3]; step SC reads set SC+2 (row j-1), writes SC+1.
     for (int j = j0; j < T.j1; j += 3) {
-        march_row<MODE, KIND, IN, LIT, 0>(A, P, T, ring, j0, j, yc, yb, raw, sbar);
+        march_row<MODE, KIND, IN, LIT, 0, SRC>(A, P, T, ring, j0, j, yc, yb, raw, sbar);
         if (j + 1 >= T.j1) break;
-        march_row<MODE, KIND, IN, LIT, 1>(A, P, T, ring, j0, j + 1, ya, yc, raw, sbar);
+        march_row<MODE, KIND, IN, LIT, 1, SRC>(A, P, T, ring, j0, j + 1, ya, yc, raw, sbar);
         if (j + 2 >= T.j1) break;
-        march_row<MODE, KIND, IN, LIT, 2>(A, P, T, ring, j0, j + 2, yb, ya, raw, sbar);
+        march_row<MODE, KIND, IN, LIT, 2, SRC>(A, P, T, ring, j0, j + 2, yb, ya, raw, sbar);
     }
     T.t0 += T.j1 - j0 + 1;  // a second pass continues the barrier phases
 }
 
-template <int MODE, int KIND, bool IN>
+template <int MODE, int KIND, bool IN, bool SRC>
 __device__ __forceinline__ void stage_body(const StageArgs& A, const KPtrs& P, double2* ring, unsigned long long* s_min,
                                            double* s_err, unsigned long long* sbar, double* s_tsc) {
     const int tid = threadIdx.x;
@@ -722,7 +725,7 @@ __device__ __forceinline__ void stage_body(const StageArgs& A, const KPtrs& P, d
     T.my_err = 0.0;
     T.t0 = 0;
     T.tsc = s_tsc;
-    if (A.source && tid == 0) stage_time_factors(A.t, s_tsc);  // read after the first row barrier
+    if (SRC && A.source && tid == 0) stage_time_factors(A.t, s_tsc);  // read after the first row barrier
 
     if (split_bar<MODE>()) {
         if (tid == 0) {
@@ -738,7 +741,7 @@ __device__ __forceinline__ void stage_body(const StageArgs& A, const KPtrs& P, d
     const bool hinted = !A.lit_all && hint && *hint;
     bool redo = A.lit_all || hinted;
     if (!redo) {
-        march_tile<MODE, KIND, IN, false>(A, P, T, ring, sbar);
+        march_tile<MODE, KIND, IN, false, SRC>(A, P, T, ring, sbar);
         redo = __syncthreads_or(guard_fail(T.gd));
     }
     bool need = false;
@@ -747,7 +750,7 @@ __device__ __forceinline__ void stage_body(const StageArgs& A, const KPtrs& P, d
         T.my_min = ~0ull;
         T.my_err = 0.0;
         T.gd = Guard();
-        march_tile<MODE, KIND, IN, true>(A, P, T, ring, sbar);
+        march_tile<MODE, KIND, IN, true, SRC>(A, P, T, ring, sbar);
         if (hint) need = __syncthreads_or(guard_fail(T.gd));
     }
     if (hint && tid == 0 && need != hinted) *hint = need;
@@ -780,7 +783,7 @@ __device__ __forceinline__ void stage_body(const StageArgs& A, const KPtrs& P, d
 // TILES 0: every tile general (IN = false); 1: every tile interior (no
 // walls, or KIND 2); 2: one launch over edge tiles (general) and interior
 // tiles (tile_mode 1, see tile_of).
-template <int MODE, int KIND, int TILES>
+template <int MODE, int KIND, int TILES, bool SRC = true>
 __global__ void __launch_bounds__(BX, min_blocks<MODE>()) sgn_stage_kernel(const StageArgs A, const KPtrs P) {
     extern __shared__ __align__(16) double2 ring[];  // 3 x NP x BX pairs
     __shared__ unsigned long long s_min[BX / 32];
@@ -790,9 +793,9 @@ __global__ void __launch_bounds__(BX, min_blocks<MODE>()) sgn_stage_kernel(const
     __shared__ int s_skip;
     if (halted(A, &s_skip)) return;
     if (TILES == 1 || (TILES == 2 && !edge_cta(A)))
-        stage_body<MODE, KIND, true>(A, P, ring, s_min, s_err, sbar, s_tsc);
+        stage_body<MODE, KIND, true, SRC>(A, P, ring, s_min, s_err, sbar, s_tsc);
     else
-        stage_body<MODE, KIND, false>(A, P, ring, s_min, s_err, sbar, s_tsc);
+        stage_body<MODE, KIND, false, SRC>(A, P, ring, s_min, s_err, sbar, s_tsc);
 }
 
 // Fused kernels: memory row of -GHOST <= jr < ny + GHOST, counted from row
@@ -861,8 +864,10 @@ __device__ __forceinline__ S12Geo s12_geo(const StageArgs& A) {
     G.xl = !PER && A.x_bounded && i == 0;
     G.xr = !PER && A.x_bounded && i == nx - 1;
     G.cx = (G.xl || G.xr) ? A.c1x : A.cpx;
-    G.sl = G.xl ? tid : tid - 1;
-    G.sr = G.xr ? tid : tid + 1;
+    // (clamped at the tile edge: the edge threads never finish a node, and
+    // the steady march reads their ring columns in bounds)
+    G.sl = (G.xl || tid == 0) ? tid : tid - 1;
+    G.sr = (G.xr || tid == BX - 1) ? tid : tid + 1;
     G.j0 = A.band0 + by * A.rows_per_block;
     G.j1 = min(A.band1 > 0 ? A.band1 : ny, G.j0 + A.rows_per_block);
     G.jc0 = (!PER && A.y_lo == YE_CLAMP) ? 0 : INT_MIN;
@@ -911,7 +916,7 @@ __device__ __forceinline__ void s12_march(const StageArgs& A, const KPtrs& P, do
         YQ ya;
         double rhac;
         {
-            const bool ok = products<MODE_S1, KIND, false>(A, raw, pc + tid, ya, gd, &rhac);
+            const bool ok = products<MODE_S1, KIND, LIT, false>(A, raw, pc + tid, ya, gd, &rhac);
             if (G.fb && r >= j0 && r < j1 && !ok) atomicAdd(&acc.bad[0], 1u);
         }
         unsigned off_rp1 = 0u;
@@ -944,7 +949,7 @@ __device__ __forceinline__ void s12_march(const StageArgs& A, const KPtrs& P, do
             const double cy = (j == G.jc0 || j == G.jc1) ? A.c1y : A.cpy;
             double k2[5];
             tendency<KIND, false, SRC, IN, LIT>(A, pb, tid, G.sl, G.sr, G.cx, cy, G.xl, G.xr, i, j, yp,
-                                                hi ? yc : ya, rhap, k2, s_tsc);
+                                                hi ? yc : ya, rhap, k2, gd, s_tsc);
             double q[5];
 #pragma unroll
             for (int f = 0; f < 5; ++f) {
@@ -956,7 +961,7 @@ __device__ __forceinline__ void s12_march(const StageArgs& A, const KPtrs& P, do
 #pragma unroll
                 for (int f = 0; f < 5; ++f) P.part[f][offe] = dadd(dmul(A.d1, kj[f]), dmul(A.d2, k2[f]));
             }
-            const bool ok = products_q<KIND, false>(q, pb[tid + P_EB * BX].y, qc + tid, yb, &rhbc, gd);
+            const bool ok = products_q<KIND, LIT, false>(q, pb[tid + P_EB * BX].y, qc + tid, yb, &rhbc, gd);
             if (G.fb && j >= j0 && j < j1 && !ok) atomicAdd(&acc.bad[1], 1u);
         }
         // ---- H2: k3 at row r-2 -> ynew (stored, min h)
@@ -975,7 +980,7 @@ __device__ __forceinline__ void s12_march(const StageArgs& A, const KPtrs& P, do
             }
             double k3[5];
             tendency<KIND, false, SRC, IN, LIT>(A, qb, tid, G.sl, G.sr, G.cx, cy, G.xl, G.xr, i, j, yp,
-                                                hi ? yc : yb, rhbp, k3, s_tsc + 2);
+                                                hi ? yc : yb, rhbp, k3, gd, s_tsc + 2);
 #pragma unroll
             for (int f = 0; f < 5; ++f) P.out[f][off] = dadd(partp[f], dmul(A.c3, k3[f]));  // state_add3
             if (ADAPT) {  // ((d1 k1 + d2 k2) + d3 k3) (time_integration.hpp:128-129)
@@ -1199,6 +1204,14 @@ static cudaError_t launch_mode(const StageArgs& A, cudaStream_t st) {
     }
     P.b = A.b - g;
     constexpr int T0 = KIND == 2 ? 1 : 0, T2 = KIND == 2 ? 1 : 2;  // KIND 2: one instance
+    // the fixed-step stage 3 without a source term: an instance without the
+    // source call region (the other modes keep the runtime test)
+    if (MODE == MODE_S3 && !A.source) {
+        static unsigned long long opted_ns[3] = {0, 0, 0};
+        return launch_planned<KIND>(A, P, sgn_stage_kernel<MODE, KIND, T0, false>,
+                                    sgn_stage_kernel<MODE, KIND, 1, false>, sgn_stage_kernel<MODE, KIND, T2, false>,
+                                    opted_ns, bytes, WX, 1, 0, st);
+    }
     return launch_planned<KIND>(A, P, sgn_stage_kernel<MODE, KIND, T0>, sgn_stage_kernel<MODE, KIND, 1>,
                                 sgn_stage_kernel<MODE, KIND, T2>, opted, bytes, WX, 1, 0, st);
 }

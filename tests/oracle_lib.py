@@ -284,3 +284,11 @@ def random_state(n: int, seed: int, lo=0.5, hi=1.5) -> np.ndarray:
     u, v, w = rng.uniform(-1, 1, (3, n))
     e = rng.uniform(lo, hi, n)
     return np.concatenate([h, u, v, w, e])
+
+
+def same_bits(a, b) -> bool:
+    """Bit-for-bit equality of two fp64 arrays (distinguishes -0.0 from +0.0
+    and compares NaN payloads), stricter than IEEE ==."""
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    return a.shape == b.shape and np.array_equal(a.view(np.uint64), b.view(np.uint64))

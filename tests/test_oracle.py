@@ -13,7 +13,8 @@ import os
 import numpy as np
 import pytest
 
-from oracle_lib import (Oracle, Phys, default_cfg, make_grid, mms_exact_field, random_state, ref_available)
+from oracle_lib import (Oracle, Phys, default_cfg, make_grid, mms_exact_field, random_state, ref_available,
+                        same_bits)
 
 GOLD = os.path.join(os.path.dirname(__file__), "golden", "golden_r1.npz")
 
@@ -53,7 +54,7 @@ def test_golden_rhs_bitwise(orc, gold):
         if source:  # independently derived source closed form: ~1e-15 relative
             assert np.max(np.abs(out - want)) <= 1e-13 * np.max(np.abs(want)), name
         else:
-            assert np.array_equal(out, want), name
+            assert same_bits(out, want), name
 
 
 def test_golden_fixed_step_bitwise(orc, gold):
@@ -64,7 +65,7 @@ def test_golden_fixed_step_bitwise(orc, gold):
                            default_cfg(fixed_dt=dt))
         r = gold[f"fixed/{kind}/rec"]
         assert (rec.t, rec.accepted, rec.rejected, rec.rhs_evals) == (r[0], r[1], r[2], r[3])
-        assert np.array_equal(q, gold[f"fixed/{kind}/q"])
+        assert same_bits(q, gold[f"fixed/{kind}/q"])
 
 
 def test_golden_adaptive_bitwise(orc, gold):
@@ -73,7 +74,7 @@ def test_golden_adaptive_bitwise(orc, gold):
                        default_cfg())
     r = gold["adaptive/rec"]
     assert (rec.t, rec.accepted, rec.rejected, rec.rhs_evals, rec.rhs_evals_setup) == tuple(r[:5])
-    assert np.array_equal(q, gold["adaptive/q"])
+    assert same_bits(q, gold["adaptive/q"])
 
 
 def test_golden_diagnostics(orc, gold):
@@ -94,7 +95,7 @@ def test_golden_init_auxiliary(orc, gold):
         b = gold[f"rhs/lake_at_rest{kind}/b"]
         q = np.zeros(5 * 33 * 33)
         q[: 33 * 33] = 1.0 - b
-        assert np.array_equal(orc.init_auxiliary(g, b, q), gold[f"init_aux/lake{kind}/q"])
+        assert same_bits(orc.init_auxiliary(g, b, q), gold[f"init_aux/lake{kind}/q"])
 
 
 def test_golden_manufactured_kats(orc, gold):
