@@ -828,6 +828,13 @@ __device__ __forceinline__ int map_row2(const StageArgs& A, int jr) {
 #define HSGN_S12_MINB (12 / (BX / 32))
 #endif
 
+// March unrolled by 2 (r2: S12 2.88 -> 2.81 ms periodic, 3.25 -> 3.20 walls;
+// by 3 within noise of 2; not unrolled, the slot pointers rotate in registers)
+#ifndef HSGN_S12_UNROLL
+#define HSGN_S12_UNROLL 2
+#endif
+constexpr int S12_UNROLL = HSGN_S12_UNROLL;
+
 // Per-thread constants of an S12 tile.
 struct S12Geo {
     int tid, i, j0, j1, jc0, jc1, sl, sr;
@@ -910,7 +917,7 @@ __device__ __forceinline__ void s12_march(const StageArgs& A, const KPtrs& P, do
     // memory offsets of rows r and r-1 (mapped once, when row r is prefetched)
     unsigned off_r = (unsigned)map_row2(A, j0 - 2) * unx + col, off_rm1 = 0u;
     load_raw<MODE_S1>(P, off_r, raw);
-#pragma unroll 1
+#pragma unroll S12_UNROLL
     for (int r = j0 - 2; r <= j1 + 1; ++r, ++k) {
         // ---- P1: stage-1 input of row r (raw of row r+1 loaded right after)
         YQ ya;
