@@ -56,8 +56,8 @@ OWN_BYTES_PER_NODE = {"S12": 128, "S3": 88}  # y, k1, b -> ynew; yn
 POINT_STAGES_PER_NODE = {"S12": 2, "S3": 1}
 # FP64 instructions (DADD + DMUL + DFMA) per node of each kernel, from the ncu
 # SASS mixes in profiles/ (the compute roofline of the FP64-issue-bound kernels)
-FP64_PER_NODE = {"S12": 437.5, "S3": 190.1}
-FP64_SOURCE = "profiles/r2_sass_mix_s12.txt, profiles/r2_sass_mix_s3.txt"
+FP64_PER_NODE = {"S12": 420.4, "S3": 180.7}
+FP64_SOURCE = "profiles/r2f_sass_mix_s12.txt, profiles/r2f_sass_mix_s3.txt"
 FP64_LANES_PER_SM, N_SM = 64, 148
 METRIC = "grid-point RK-stage updates/sec on 8192² fp64 grid; achieved HBM GB/s"
 UNIT = "point-stage updates/s"
