@@ -4,6 +4,8 @@ per-stage halo exchange) on ONE B200: n slab contexts in one process
 schedule the NCCL path runs across GPUs.  Required: bitwise equality with the
 single-context run (the RHS has no reductions), and decomposition-independent
 SBP-norm diagnostics (row sums combined in global row order)."""
+import ctypes as C
+
 import numpy as np
 import pytest
 
@@ -61,3 +63,36 @@ def test_group_with_manufactured_source_and_walls():
     grp.rhs(0.0, gy, go)
     assert np.count_nonzero(grp.download(go) != out.flat()) == 0
     grp.close()
+
+
+def test_group_halts_when_one_slab_goes_dry():
+    """A depth failure that only one slab sees (a draining hole inside slab
+    0 of 3) halts every slab at the same step: the steps done and the last
+    valid state equal the single-context run's (a failure local
+    to one slab must not let the other slabs step on)."""
+    nx, ny, n = 64, 48, 3
+    x = -1 + np.arange(nx) * 2 / nx
+    y = -1 + np.arange(ny) * 2 / ny
+    X, Y = np.meshgrid(x, y)
+    e = np.exp(-(X ** 2 + (Y + 0.7) ** 2) / 0.02)
+    h = 1 - 0.99 * e
+    q = np.concatenate([h.ravel(), (10 * X * e).ravel(), (10 * (Y + 0.7) * e).ravel(), np.zeros(nx * ny),
+                        h.ravel()])
+    g = H.make_grid(-1.0, 1.0, -1.0, 1.0, nx, ny)
+    phys = H.PhysSetup(9.81, 500.0, 1e-12, np.zeros((ny, nx)))
+    dt, steps = 1e-3, 200
+    ctx = H.make_rhs_context(g, phys)
+    a = H.adaptive_solve(ctx, H.StateField(g, q), 0.0, steps * dt, H.IntegratorConfig(fixed_dt=dt))
+    assert a.aborted and 0 < a.accepted < steps
+
+    N = H.api.N
+    grp = S.SlabGroup(g, phys, n)
+    gy, gk = grp.state(q), grp.state()
+    grp.rhs(0.0, gy, gk)
+    done = C.c_int64(0)
+    st = N.lib().hsgn_group_bs3_fixed_steps(grp._h, gy, gk, 0.0, dt, steps, C.byref(done))
+    assert st == N.HSGN_EDEPTH
+    assert done.value == a.accepted
+    assert np.count_nonzero(grp.download(gy) != a.q.flat()) == 0
+    grp.close()
+    ctx.close()
