@@ -149,23 +149,6 @@ __device__ __forceinline__ void load_raw(const KPtrs& P, unsigned off, Raw& r) {
     r.b = __ldg(P.b + off);
 }
 
-// L2 prefetch of a raw row one row beyond the register prefetch
-// (experiment switch HSGN_L2PF: 1 stage kernels, 2 S12, 3 both)
-#ifndef HSGN_L2PF
-#define HSGN_L2PF 0
-#endif
-template <int MODE>
-__device__ __forceinline__ void prefetch_raw_l2(const KPtrs& P, unsigned off) {
-    auto pf = [](const double* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); };
-#pragma unroll
-    for (int f = 0; f < 5; ++f) pf(P.y[f] + off);
-    if (MODE == MODE_S1 || MODE == MODE_S2) {
-#pragma unroll
-        for (int f = 0; f < 5; ++f) pf(P.k[f] + off);
-    }
-    pf(P.b + off);
-}
-
 // Pointwise products of rhs.hpp:99-109 at one node from the stage input q
 // (h, u, v, w, eta) and b: stores the ring pairs of the node (S already
 // offset by ring row and column), fills the y-quantities and the node's
@@ -597,7 +580,6 @@ __device__ __forceinline__ void march_row(const StageArgs& A, const KPtrs& P, Th
     }
     // register prefetch of raw(jn+1), in flight during the finish of row j
     if (jn < T.j1) load_raw<MODE>(P, (unsigned)map_row(A, jn + 1) * nx + T.col, raw);
-    if ((HSGN_L2PF & 1) && jn + 1 < T.j1) prefetch_raw_l2<MODE>(P, (unsigned)map_row(A, jn + 2) * nx + T.col);
     // One barrier per row: row j's ring entries (written one step ago) become
     // visible, and this step's writes to slot SN are ordered after the last
     // reads of that slot (finish of row j-2, before the previous barrier).
@@ -948,7 +930,6 @@ __device__ __forceinline__ void s12_march(const StageArgs& A, const KPtrs& P, do
         if (r + 1 <= j1 + 1) {
             off_rp1 = (unsigned)map_row2(A, r + 1) * unx + col;
             load_raw<MODE_S1>(P, off_rp1, raw);
-            if ((HSGN_L2PF & 2) && r + 2 <= j1 + 1) prefetch_raw_l2<MODE_S1>(P, (unsigned)map_row2(A, r + 2) * unx + col);
         }
         // H1's own-column inputs need no barrier: they are requested before
         // the wait (this thread loaded them one row ago: L1/L2 hits)
