@@ -834,6 +834,19 @@ __device__ __forceinline__ int map_row2(const StageArgs& A, int jr) {
 #define HSGN_S12_UNROLL 2
 #endif
 constexpr int S12_UNROLL = HSGN_S12_UNROLL;
+#ifndef HSGN_S12_FLAT
+#define HSGN_S12_FLAT 2
+#endif
+// FLAT: one branch-free iteration body (H1 and H2 evaluated on every thread
+// and iteration, stores / counters / guard predicated on valid rows).
+// HSGN_S12_FLAT 0: no instance; 1: every instance; 2 (default): the adaptive
+// and sourced instances.  Measured (r2): it removes most of the spills of the
+// adaptive / sourced instances (e.g. 592 -> 0 B) and makes the sourced
+// config-2 attempt 4-5 % faster (4096^2: 2.50-2.55 -> 2.37 ms); adaptive
+// neutral; the plain fixed-step instances are 2-3 % slower flat (S12 2.81 ->
+// 2.87 ms periodic, 3.12 -> 3.21 walls), so they keep the branched body.
+template <bool ADAPT, bool SRC>
+__host__ __device__ constexpr bool s12_flat() { return HSGN_S12_FLAT == 1 || (HSGN_S12_FLAT == 2 && (ADAPT || SRC)); }
 
 // Per-thread constants of an S12 tile.
 struct S12Geo {
@@ -893,6 +906,7 @@ __device__ __forceinline__ S12Geo s12_geo(const StageArgs& A) {
 template <int KIND, bool ADAPT, bool SRC, bool IN, bool LIT>
 __device__ __forceinline__ void s12_march(const StageArgs& A, const KPtrs& P, double2* ring,
                                           unsigned long long* s_bar, int& k, S12Acc& acc, const double* s_tsc) {
+    constexpr bool FLAT = s12_flat<ADAPT, SRC>();
     const S12Geo G = s12_geo<KIND, IN>(A);
     const int tid = G.tid, i = G.i, j0 = G.j0, j1 = G.j1, ny = A.ny;
     const unsigned unx = (unsigned)A.nx, col = G.col;
@@ -914,6 +928,7 @@ __device__ __forceinline__ void s12_march(const StageArgs& A, const KPtrs& P, do
     // next stage-1 input while the others finish.  (Measured slower: a
     // second barrier set with a 4-slot ring B, 2.68 vs 2.63 ms.)
     Raw raw;
+    unsigned n1 = 0u, n2 = 0u;  // FLAT: depth failures of stage inputs 1, 2 on this thread's finished nodes
     // memory offsets of rows r and r-1 (mapped once, when row r is prefetched)
     unsigned off_r = (unsigned)map_row2(A, j0 - 2) * unx + col, off_rm1 = 0u;
     load_raw<MODE_S1>(P, off_r, raw);
@@ -924,10 +939,16 @@ __device__ __forceinline__ void s12_march(const StageArgs& A, const KPtrs& P, do
         double rhac;
         {
             const bool ok = products<MODE_S1, KIND, LIT, false>(A, raw, pc + tid, ya, gd, &rhac);
-            if (G.fb && r >= j0 && r < j1 && !ok) atomicAdd(&acc.bad[0], 1u);
+            if (FLAT)
+                n1 += (G.fb && r >= j0 && r < j1 && !ok) ? 1u : 0u;
+            else if (G.fb && r >= j0 && r < j1 && !ok)
+                atomicAdd(&acc.bad[0], 1u);
         }
         unsigned off_rp1 = 0u;
-        if (r + 1 <= j1 + 1) {
+        if (FLAT) {  // the last iteration reloads row j1 + 1 (never read)
+            off_rp1 = (unsigned)map_row2(A, min(r + 1, j1 + 1)) * unx + col;
+            load_raw<MODE_S1>(P, off_rp1, raw);
+        } else if (r + 1 <= j1 + 1) {
             off_rp1 = (unsigned)map_row2(A, r + 1) * unx + col;
             load_raw<MODE_S1>(P, off_rp1, raw);
         }
@@ -935,7 +956,7 @@ __device__ __forceinline__ void s12_march(const StageArgs& A, const KPtrs& P, do
         // the wait (this thread loaded them one row ago: L1/L2 hits)
         const bool do1 = r - 1 >= j0 - 1 && G.fa;
         double yj[5], kj[5];
-        if (do1) {
+        if (FLAT || do1) {
             const unsigned offj = off_rm1;
 #pragma unroll
             for (int f = 0; f < 5; ++f) {
@@ -947,7 +968,7 @@ __device__ __forceinline__ void s12_march(const StageArgs& A, const KPtrs& P, do
         // ---- H1: k2 at row r-1 -> stage-2 input -> ring B (qc)
         YQ yb;
         double rhbc = 0.0, partc[5];
-        if (do1) {
+        if (FLAT || do1) {
             const int j = r - 1;
             YQ yp, yc;
             neighbour_y((G.clamp_lo && j == 0 ? pb : pa) + tid, yp);  // a clamped wall row reads itself
@@ -955,8 +976,9 @@ __device__ __forceinline__ void s12_march(const StageArgs& A, const KPtrs& P, do
             if (hi) neighbour_y(pb + tid, yc);
             const double cy = (j == G.jc0 || j == G.jc1) ? A.c1y : A.cpy;
             double k2[5];
+            Guard g1;
             tendency<KIND, false, SRC, IN, LIT>(A, pb, tid, G.sl, G.sr, G.cx, cy, G.xl, G.xr, i, j, yp,
-                                                hi ? yc : ya, rhap, k2, gd, s_tsc);
+                                                hi ? yc : ya, rhap, k2, FLAT ? g1 : gd, s_tsc);
             double q[5];
 #pragma unroll
             for (int f = 0; f < 5; ++f) {
@@ -968,11 +990,18 @@ __device__ __forceinline__ void s12_march(const StageArgs& A, const KPtrs& P, do
 #pragma unroll
                 for (int f = 0; f < 5; ++f) P.part[f][offe] = dadd(dmul(A.d1, kj[f]), dmul(A.d2, k2[f]));
             }
-            const bool ok = products_q<KIND, LIT, false>(q, pb[tid + P_EB * BX].y, qc + tid, yb, &rhbc, gd);
-            if (G.fb && j >= j0 && j < j1 && !ok) atomicAdd(&acc.bad[1], 1u);
+            const bool ok =
+                products_q<KIND, LIT, false>(q, pb[tid + P_EB * BX].y, qc + tid, yb, &rhbc, FLAT ? g1 : gd);
+            if (FLAT) {
+                n2 += (G.fb && j >= j0 && j < j1 && !ok) ? 1u : 0u;
+                guard_merge(gd, g1, do1);
+            } else if (G.fb && j >= j0 && j < j1 && !ok) {
+                atomicAdd(&acc.bad[1], 1u);
+            }
         }
         // ---- H2: k3 at row r-2 -> ynew (stored, min h)
-        if (r - 2 >= j0 && G.fb) {
+        const bool do2 = r - 2 >= j0 && G.fb;
+        if (FLAT || do2) {
             const int j = r - 2;
             YQ yp, yc;
             neighbour_y((G.clamp_lo && j == 0 ? qb : qa) + tid, yp);
@@ -981,22 +1010,28 @@ __device__ __forceinline__ void s12_march(const StageArgs& A, const KPtrs& P, do
             const double cy = (j == G.jc0 || j == G.jc1) ? A.c1y : A.cpy;
             const unsigned off = (unsigned)(j + GHOST) * unx + col;
             double e12[5];  // ADAPT: d1 k1 + d2 k2 stored by H1 one row ago (requested before the tendency)
-            if (ADAPT) {
+            if (ADAPT && do2) {
 #pragma unroll
                 for (int f = 0; f < 5; ++f) e12[f] = P.part[f][off];
             }
             double k3[5];
+            Guard g2;
             tendency<KIND, false, SRC, IN, LIT>(A, qb, tid, G.sl, G.sr, G.cx, cy, G.xl, G.xr, i, j, yp,
-                                                hi ? yc : yb, rhbp, k3, gd, s_tsc + 2);
+                                                hi ? yc : yb, rhbp, k3, FLAT ? g2 : gd, s_tsc + 2);
+            if (FLAT) guard_merge(gd, g2, do2);
+            double yn[5];
 #pragma unroll
-            for (int f = 0; f < 5; ++f) P.out[f][off] = dadd(partp[f], dmul(A.c3, k3[f]));  // state_add3
-            if (ADAPT) {  // ((d1 k1 + d2 k2) + d3 k3) (time_integration.hpp:128-129)
+            for (int f = 0; f < 5; ++f) yn[f] = dadd(partp[f], dmul(A.c3, k3[f]));  // state_add3
+            if (do2) {
 #pragma unroll
-                for (int f = 0; f < 5; ++f) P.part[f][off] = dadd(e12[f], dmul(A.d3, k3[f]));
+                for (int f = 0; f < 5; ++f) P.out[f][off] = yn[f];
+                if (ADAPT) {  // ((d1 k1 + d2 k2) + d3 k3) (time_integration.hpp:128-129)
+#pragma unroll
+                    for (int f = 0; f < 5; ++f) P.part[f][off] = dadd(e12[f], dmul(A.d3, k3[f]));
+                }
             }
-            const unsigned long long bits =
-                (unsigned long long)__double_as_longlong(dadd(partp[0], dmul(A.c3, k3[0])));
-            acc.my_min = bits < acc.my_min ? bits : acc.my_min;
+            const unsigned long long bits = (unsigned long long)__double_as_longlong(yn[0]);
+            acc.my_min = (do2 && bits < acc.my_min) ? bits : acc.my_min;
         }
         mbar_arrive(&s_bar[k & 1]);
         // ---- rotate
@@ -1014,6 +1049,10 @@ __device__ __forceinline__ void s12_march(const StageArgs& A, const KPtrs& P, do
         off_r = off_rp1;
 #pragma unroll
         for (int f = 0; f < 5; ++f) partp[f] = partc[f];
+    }
+    if (FLAT) {
+        if (n1) atomicAdd(&acc.bad[0], n1);
+        if (n2) atomicAdd(&acc.bad[1], n2);
     }
     acc.any = guard_fail(gd);
 }
